@@ -1,0 +1,97 @@
+"""paper_2402_15253_b200 -- B200-native k-core decomposition (PICO,
+arXiv 2402.15253): HistoCore (Alg 6) and PeelOne (Alg 4, PO-dyn) as
+hand-written sm_100a CUDA behind the C ABI of include/pico.h.
+
+Python is a thin ctypes layer (argument marshalling only).  PyTorch supplies
+device memory, streams and process groups.  There is no CPU fallback: on a
+machine without the built library or without a GPU every compute call raises.
+
+    import paper_2402_15253_b200 as pico
+    core = pico.coreness(rowptr_cuda_int64, colidx_cuda_int32, algo="histocore")
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from ._lib import (ALGOS, F_CLAMP_SUB, F_HOST_LOOP, F_STATS, F_TIMING, F_TINY_TILES,  # noqa: F401
+                   F_VALIDATE, PicoError, Stats, check, header_functions, load)
+
+__all__ = ["coreness", "coreness_host", "workspace_bytes", "PicoError", "Stats", "load",
+           "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES"]
+
+
+def _algo(algo) -> int:
+    if isinstance(algo, str):
+        if algo not in ALGOS:
+            raise ValueError(f"unknown algo {algo!r}; expected one of {sorted(ALGOS)}")
+        return ALGOS[algo]
+    return int(algo)
+
+
+def workspace_bytes(n: int, m: int, algo="histocore", flags: int = 0) -> int:
+    return int(load().pico_workspace_bytes(n, m, _algo(algo), flags))
+
+
+def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspace=None,
+             stats: Stats | None = None, frontier_sizes=None, stream=None):
+    """Coreness of every vertex of a symmetric deduplicated CSR graph held in
+    device memory (``pico_coreness_ex``).
+
+    rowptr: int64 CUDA tensor [n+1]; colidx: int32 CUDA tensor [2m].
+    Returns an int32 CUDA tensor [n].  ``stats`` (a :class:`Stats`) is filled
+    in place; ``frontier_sizes`` an optional int64 numpy array receiving
+    |F_t| per round (HistoCore) or vertices per level (PeelOne).
+    """
+    import torch
+    lib = load()
+    if not (rowptr.is_cuda and colidx.is_cuda):
+        raise ValueError("rowptr and colidx must be CUDA tensors (no CPU fallback)")
+    if rowptr.dtype != torch.int64 or colidx.dtype != torch.int32:
+        raise TypeError("rowptr must be int64 and colidx int32")
+    rowptr = rowptr.contiguous()
+    colidx = colidx.contiguous()
+    n = rowptr.numel() - 1
+    arcs = colidx.numel()
+    if arcs % 2:
+        raise ValueError("colidx length must be even (2m arcs of a symmetric graph)")
+    m = arcs // 2
+    if out is None:
+        out = torch.empty(max(n, 0), dtype=torch.int32, device=rowptr.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(rowptr.device)
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    st = stats
+    if frontier_sizes is not None:
+        if st is None:
+            st = Stats()
+        st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        st.frontier_sizes_cap = frontier_sizes.size
+    with torch.cuda.device(rowptr.device):
+        rc = lib.pico_coreness_ex(rowptr.data_ptr(), colidx.data_ptr() if arcs else None, n, m, _algo(algo),
+                                  out.data_ptr() if n > 0 else None, ctypes.c_void_p(stream.cuda_stream), flags,
+                                  ws_ptr, ws_bytes, ctypes.byref(st) if st is not None else None)
+    check(rc)
+    return out
+
+
+def coreness_host(rowptr: np.ndarray, colidx: np.ndarray, algo="histocore", flags: int = 0, out=None,
+                  stats: Stats | None = None, stream=None) -> np.ndarray:
+    """End-to-end call on HOST arrays (``pico_coreness_host``): H2D copies,
+    the CUDA path, D2H of the coreness -- all inside the library call."""
+    lib = load()
+    rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+    ci = np.ascontiguousarray(colidx, dtype=np.int32)
+    n = rp.size - 1
+    m = ci.size // 2
+    if out is None:
+        out = np.empty(max(n, 0), dtype=np.int32)
+    sptr = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+    rc = lib.pico_coreness_host(rp.ctypes.data, ci.ctypes.data if ci.size else None, n, m, _algo(algo),
+                                out.ctypes.data if n > 0 else None, sptr, flags,
+                                ctypes.byref(stats) if stats is not None else None)
+    check(rc)
+    return out

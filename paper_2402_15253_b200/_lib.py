@@ -1,0 +1,136 @@
+"""ctypes binding of libpico.so -- argument marshalling only.  Every step of
+the coreness computation runs in the library's CUDA kernels; there is no
+Python or CPU fallback: if the library cannot be loaded, or no GPU is
+present, calls raise."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+from .build import INCLUDE, LIB
+
+ALGOS = {"histocore": 0, "peelone": 1}
+
+F_VALIDATE = 1
+F_STATS = 2
+F_TIMING = 4
+F_HOST_LOOP = 8
+F_CLAMP_SUB = 16
+F_TINY_TILES = 32
+
+K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "other"]
+
+STATUS = {0: "PICO_OK", 1: "PICO_EINVAL", 2: "PICO_ENOTSUP", 3: "PICO_ENOMEM",
+          4: "PICO_ECUDA", 5: "PICO_ENCCL", 6: "PICO_EGRAPH"}
+
+
+class PicoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.msg = msg
+
+
+class Stats(ctypes.Structure):
+    """Mirror of pico_stats_t (include/pico.h)."""
+    _fields_ = [
+        ("rounds", ctypes.c_int64),
+        ("levels", ctypes.c_int64),
+        ("subrounds", ctypes.c_int64),
+        ("kmax", ctypes.c_int64),
+        ("frontier_total", ctypes.c_int64),
+        ("init_slots_written", ctypes.c_int64),
+        ("arcs_scanned", ctypes.c_int64),
+        ("guarded_arcs", ctypes.c_int64),
+        ("bins_read", ctypes.c_int64),
+        ("pushes", ctypes.c_int64),
+        ("alive_scanned", ctypes.c_int64),
+        ("hub_fallbacks", ctypes.c_int64),
+        ("kernel_ms", ctypes.c_double * 8),
+        ("kernel_launches", ctypes.c_int64 * 8),
+        ("frontier_sizes", ctypes.POINTER(ctypes.c_int64)),
+        ("frontier_sizes_cap", ctypes.c_int64),
+    ]
+
+    def to_dict(self) -> dict:
+        d = {k: int(getattr(self, k)) for k, _ in self._fields_[:12]}
+        d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(8) if self.kernel_launches[i]}
+        d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(8) if self.kernel_launches[i]}
+        return d
+
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Every function declared in include/*.h (for the export test)."""
+    names = []
+    for fn in sorted(os.listdir(INCLUDE)):
+        if not fn.endswith(".h"):
+            continue
+        txt = open(os.path.join(INCLUDE, fn)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s*(pico_[A-Za-z0-9_]+)\s*\(",
+                             txt, flags=re.M):
+            names.append(m.group(1))
+    return sorted(set(names))
+
+
+def load(path: str | None = None):
+    """Load libpico.so (raises OSError if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB
+    if not os.path.exists(p):
+        raise OSError(f"libpico.so not built ({p}); run `python -m paper_2402_15253_b200.build` "
+                      "or __graft_entry__.build()")
+    lib = ctypes.CDLL(p)
+    vp, i64, i32, u32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint32, ctypes.c_size_t
+    lib.pico_coreness.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+    lib.pico_coreness.restype = i32
+    lib.pico_workspace_bytes.argtypes = [i64, i64, i32, u32]
+    lib.pico_workspace_bytes.restype = sz
+    lib.pico_coreness_ex.argtypes = [vp, vp, i64, i64, i32, vp, vp, u32, vp, sz, ctypes.POINTER(Stats)]
+    lib.pico_coreness_ex.restype = i32
+    lib.pico_coreness_host.argtypes = [vp, vp, i64, i64, i32, vp, vp, u32, ctypes.POINTER(Stats)]
+    lib.pico_coreness_host.restype = i32
+    lib.pico_status_string.argtypes = [i32]
+    lib.pico_status_string.restype = ctypes.c_char_p
+    lib.pico_last_error.argtypes = []
+    lib.pico_last_error.restype = ctypes.c_char_p
+    lib.pico_version.argtypes = []
+    lib.pico_version.restype = i32
+    _setup_shard(lib)
+    _lib = lib
+    return lib
+
+
+def _setup_shard(lib):
+    """Signatures of the sharded-HistoCore entry points (include/pico_shard.h)."""
+    if not hasattr(lib, "pico_shard_create"):
+        return
+    vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint32
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    lib.pico_shard_create.argtypes = [vp, vp, i64, i64, i64, vp, u32, ctypes.POINTER(vp)]
+    lib.pico_shard_create.restype = i32
+    lib.pico_shard_destroy.argtypes = [vp]
+    lib.pico_shard_destroy.restype = i32
+    lib.pico_shard_init.argtypes = [vp, vp, P64]
+    lib.pico_shard_init.restype = i32
+    lib.pico_shard_pack.argtypes = [vp, vp, vp, i64, P64]
+    lib.pico_shard_pack.restype = i32
+    lib.pico_shard_apply.argtypes = [vp, vp, i64, vp, P64]
+    lib.pico_shard_apply.restype = i32
+    lib.pico_shard_sum.argtypes = [vp, vp, P64]
+    lib.pico_shard_sum.restype = i32
+    lib.pico_shard_result.argtypes = [vp, vp, vp]
+    lib.pico_shard_result.restype = i32
+    lib.pico_shard_build_csc.argtypes = [vp, vp]
+    lib.pico_shard_build_csc.restype = i32
+
+
+def check(rc: int):
+    if rc != 0:
+        raise PicoError(rc, load().pico_last_error().decode(errors="replace"))

@@ -1,0 +1,274 @@
+// capi.cu -- the extern "C" boundary declared in include/pico.h: argument
+// checks, workspace ownership, optional CSR validation, dispatch to the
+// HistoCore / PeelOne drivers, status codes and the thread-local last error.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pico {
+
+// ---------------------------------------------------------------------------
+// PICO_F_VALIDATE: the CSR contract of pico.h
+// ---------------------------------------------------------------------------
+enum { BAD_ROWPTR = 1, BAD_RANGE = 2, BAD_LOOP = 4, BAD_ORDER = 8, BAD_ASYM = 16 };
+
+__global__ void validate_rowptr_kernel(const long long *rp, long long n, long long arcs, int *bad) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nthreads) {
+        long long a = rp[v], b = rp[v + 1];
+        if (a < 0 || b < a || b > arcs) atomicOr(bad, BAD_ROWPTR);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (rp[0] != 0 || rp[n] != arcs)) atomicOr(bad, BAD_ROWPTR);
+}
+
+__global__ void validate_arcs_kernel(const long long *rp, const int *ci, long long n, int *bad) {
+    // one warp per row
+    long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    int lane = threadIdx.x & 31;
+    int flags = 0;
+    for (long long v = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < n; v += nw) {
+        long long a = rp[v], b = rp[v + 1];
+        for (long long e = a + lane; e < b; e += 32) {
+            int u = ci[e];
+            if (u < 0 || u >= n) { flags |= BAD_RANGE; continue; }
+            if (u == v) flags |= BAD_LOOP;
+            if (e > a && ci[e - 1] >= u) flags |= BAD_ORDER;
+            // symmetry: v must appear in row u (binary search; rows sorted)
+            long long lo = rp[u], hi = rp[u + 1] - 1;
+            bool found = false;
+            while (lo <= hi) {
+                long long mid = (lo + hi) >> 1;
+                int x = ci[mid];
+                if (x == v) { found = true; break; }
+                if (x < v) lo = mid + 1; else hi = mid - 1;
+            }
+            if (!found) flags |= BAD_ASYM;
+        }
+    }
+    if (flags) atomicOr(bad, flags);
+}
+
+cudaError_t validate_run(const long long *rp, const int *ci, long long n, long long arcs, cudaStream_t s,
+                         void *ws, int *bad_out) {
+    int *bad = (int *)ws;
+    cudaError_t err;
+    if ((err = cudaMemsetAsync(bad, 0, sizeof(int), s))) return err;
+    validate_rowptr_kernel<<<1024, 256, 0, s>>>(rp, n, arcs, bad);
+    int h = 0;
+    if ((err = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s))) return err;
+    if ((err = cudaStreamSynchronize(s))) return err;
+    if (!h && arcs > 0) {
+        validate_arcs_kernel<<<2048, 256, 0, s>>>(rp, ci, n, bad);
+        if ((err = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s))) return err;
+        if ((err = cudaStreamSynchronize(s))) return err;
+    }
+    *bad_out = h;
+    return cudaGetLastError();
+}
+
+__global__ void max_kernel(const int *x, long long n, int *out) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    int m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthreads) m = max(m, x[i]);
+    m = max(m, __shfl_xor_sync(FULL, m, 16));
+    m = max(m, __shfl_xor_sync(FULL, m, 8));
+    m = max(m, __shfl_xor_sync(FULL, m, 4));
+    m = max(m, __shfl_xor_sync(FULL, m, 2));
+    m = max(m, __shfl_xor_sync(FULL, m, 1));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+}  // namespace pico
+
+using namespace pico;
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char *where) {
+    cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) return fail(PICO_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
+    return fail(PICO_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static cudaError_t dev_info(DevInfo *d) {
+    cudaError_t e;
+    if ((e = cudaGetDevice(&d->device))) return e;
+    if ((e = cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->device))) return e;
+    if ((e = cudaDeviceGetAttribute(&d->coop, cudaDevAttrCooperativeLaunch, d->device))) return e;
+    return cudaSuccess;
+}
+
+static void reset_stats(pico_stats_t *st) {
+    if (!st) return;
+    int64_t *fs = st->frontier_sizes;
+    int64_t cap = st->frontier_sizes_cap;
+    memset(st, 0, sizeof(*st));
+    st->frontier_sizes = fs;
+    st->frontier_sizes_cap = cap;
+}
+
+extern "C" {
+
+const char *pico_status_string(int status) {
+    switch (status) {
+        case PICO_OK: return "PICO_OK";
+        case PICO_EINVAL: return "PICO_EINVAL";
+        case PICO_ENOTSUP: return "PICO_ENOTSUP";
+        case PICO_ENOMEM: return "PICO_ENOMEM";
+        case PICO_ECUDA: return "PICO_ECUDA";
+        case PICO_ENCCL: return "PICO_ENCCL";
+        case PICO_EGRAPH: return "PICO_EGRAPH";
+        default: return "PICO_UNKNOWN";
+    }
+}
+
+const char *pico_last_error(void) { return g_last_error.c_str(); }
+
+int pico_version(void) { return 100; }
+
+size_t pico_workspace_bytes(int64_t n, int64_t m, int algo, uint32_t flags) {
+    if (n <= 0 || m < 0) return 256;
+    long long arcs = 2 * (long long)m;
+    size_t b = 0;
+    if (algo == PICO_ALGO_HISTOCORE) b = hc_workspace_bytes(n, arcs, flags);
+    else if (algo == PICO_ALGO_PEELONE) b = po_workspace_bytes(n, arcs, flags);
+    return std::max<size_t>(b, 256);
+}
+
+int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, int64_t m, int algo,
+                     int32_t *core_out, pico_stream_t stream_, uint32_t flags, void *workspace,
+                     size_t workspace_bytes, pico_stats_t *stats) {
+    cudaStream_t s = (cudaStream_t)stream_;
+    g_last_error.clear();
+    reset_stats(stats);
+    if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n (%lld) or m (%lld)", (long long)n, (long long)m);
+    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE)
+        return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (n == 0) return PICO_OK;
+    if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n = %lld needs 64-bit vertex ids", (long long)n);
+    if (!rowptr || !core_out || (m > 0 && !colidx)) return fail(PICO_EINVAL, "NULL pointer argument");
+    const long long arcs = 2 * (long long)m;
+    size_t need = pico_workspace_bytes(n, m, algo, flags);
+    if (workspace && workspace_bytes < need)
+        return fail(PICO_EINVAL, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    if (workspace && ((uintptr_t)workspace & 255))
+        return fail(PICO_EINVAL, "workspace must be 256-byte aligned");
+
+    DevInfo dev;
+    cudaError_t e = dev_info(&dev);
+    if (e) return cuda_fail(e, "device query");
+    void *ws = workspace;
+    bool own = false;
+    if (!ws) {
+        e = cudaMallocAsync(&ws, need, s);
+        if (e) return cuda_fail(e, "workspace allocation");
+        own = true;
+    }
+    int rc = PICO_OK;
+    const long long *rp = (const long long *)rowptr;
+    if (flags & PICO_F_VALIDATE) {
+        int bad = 0;
+        e = validate_run(rp, colidx, n, arcs, s, ws, &bad);
+        if (e) rc = cuda_fail(e, "validation");
+        else if (bad)
+            rc = fail(PICO_EGRAPH, "graph violates the CSR contract (flags 0x%x: %s%s%s%s%s)", bad,
+                      (bad & 1) ? "rowptr " : "", (bad & 2) ? "range " : "", (bad & 4) ? "self-loop " : "",
+                      (bad & 8) ? "unsorted/duplicate " : "", (bad & 16) ? "asymmetric" : "");
+    }
+    if (rc == PICO_OK) {
+        if (m == 0) {
+            e = cudaMemsetAsync(core_out, 0, sizeof(int32_t) * (size_t)n, s);
+            if (!e) e = cudaStreamSynchronize(s);
+            if (e) rc = cuda_fail(e, "zero core_out");
+        } else {
+            if (!dev.coop && !(flags & PICO_F_HOST_LOOP)) flags |= PICO_F_HOST_LOOP;
+            if (algo == PICO_ALGO_HISTOCORE)
+                e = hc_run(rp, colidx, n, arcs, core_out, s, flags, ws, stats, dev);
+            else
+                e = po_run(rp, colidx, n, arcs, core_out, s, flags, ws, stats, dev);
+            if (e) rc = cuda_fail(e, algo == PICO_ALGO_HISTOCORE ? "histocore" : "peelone");
+            if (!e && stats && algo == PICO_ALGO_HISTOCORE) {
+                int *d = (int *)ws;  // Ctrl region is free again
+                int km = 0;
+                e = cudaMemsetAsync(d, 0, sizeof(int), s);
+                if (!e) {
+                    max_kernel<<<dev.sms * 4, 256, 0, s>>>(core_out, n, d);
+                    e = cudaMemcpyAsync(&km, d, sizeof(int), cudaMemcpyDeviceToHost, s);
+                }
+                if (!e) e = cudaStreamSynchronize(s);
+                if (e) rc = cuda_fail(e, "kmax");
+                else stats->kmax = km;
+            }
+        }
+    }
+    if (own) {
+        cudaError_t e2 = cudaFreeAsync(ws, s);
+        if (!e2) e2 = cudaStreamSynchronize(s);
+        if (e2 && rc == PICO_OK) rc = cuda_fail(e2, "workspace free");
+    }
+    return rc;
+}
+
+int pico_coreness(const int64_t *rowptr, const int32_t *colidx, int64_t n, int64_t m, int algo,
+                  int32_t *core_out, pico_stream_t stream) {
+    return pico_coreness_ex(rowptr, colidx, n, m, algo, core_out, stream, 0u, nullptr, 0, nullptr);
+}
+
+int pico_coreness_host(const int64_t *rowptr_h, const int32_t *colidx_h, int64_t n, int64_t m, int algo,
+                       int32_t *core_out_h, pico_stream_t stream_, uint32_t flags, pico_stats_t *stats) {
+    cudaStream_t s = (cudaStream_t)stream_;
+    g_last_error.clear();
+    reset_stats(stats);
+    if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n or m");
+    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE)
+        return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (n == 0) return PICO_OK;
+    if (!rowptr_h || !core_out_h || (m > 0 && !colidx_h)) return fail(PICO_EINVAL, "NULL pointer argument");
+    if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n too large");
+    const size_t arcs = 2 * (size_t)m;
+    void *d_rp = nullptr, *d_ci = nullptr, *d_core = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_rp, sizeof(int64_t) * (size_t)(n + 1), s);
+    if (!e) e = cudaMallocAsync(&d_ci, sizeof(int32_t) * std::max<size_t>(arcs, 1), s);
+    if (!e) e = cudaMallocAsync(&d_core, sizeof(int32_t) * (size_t)n, s);
+    int rc = PICO_OK;
+    if (e) rc = cuda_fail(e, "device buffers");
+    if (rc == PICO_OK) {
+        e = cudaMemcpyAsync(d_rp, rowptr_h, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, s);
+        if (!e && arcs) e = cudaMemcpyAsync(d_ci, colidx_h, sizeof(int32_t) * arcs, cudaMemcpyHostToDevice, s);
+        if (e) rc = cuda_fail(e, "host to device copy");
+    }
+    if (rc == PICO_OK) {
+        std::string keep;
+        rc = pico_coreness_ex((const int64_t *)d_rp, (const int32_t *)d_ci, n, m, algo, (int32_t *)d_core, stream_,
+                              flags, nullptr, 0, stats);
+        if (rc != PICO_OK) keep = g_last_error;
+        if (rc == PICO_OK) {
+            e = cudaMemcpyAsync(core_out_h, d_core, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, s);
+            if (e) rc = cuda_fail(e, "device to host copy");
+        } else {
+            g_last_error = keep;
+        }
+    }
+    if (d_rp) cudaFreeAsync(d_rp, s);
+    if (d_ci) cudaFreeAsync(d_ci, s);
+    if (d_core) cudaFreeAsync(d_core, s);
+    e = cudaStreamSynchronize(s);
+    if (e && rc == PICO_OK) rc = cuda_fail(e, "synchronize");
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// common.cuh -- device helpers shared by the HistoCore and PeelOne kernels
+// (sm_100a).  Warp-aggregated list appends (ballot/popc compaction), warp
+// scans, a software grid barrier for the persistent cooperative kernels, and
+// the workspace control block.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pico {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// inclusive warp scan (sum) of a 32-bit value
+__device__ __forceinline__ int warp_incl_scan(int x) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ long long warp_incl_scan64(long long x) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ long long warp_sum64(long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
+__device__ __forceinline__ int warp_min(int x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(FULL, x, o));
+    return x;
+}
+
+// Warp-aggregated append of `v` (for lanes with pred) to list/count.  Must be
+// called by all 32 lanes of the warp.  One atomic per warp; slots in lane
+// order (ballot + popc compaction).
+__device__ __forceinline__ void warp_append(bool pred, int v, int *list,
+                                            unsigned long long *count) {
+    unsigned m = __ballot_sync(FULL, pred);
+    if (m == 0) return;
+    unsigned long long base = 0;
+    int leader = __ffs(m) - 1;
+    if (lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(FULL, base, leader);
+    if (pred) list[base + __popc(m & ((1u << lane_id()) - 1))] = v;
+}
+
+// relaxed/volatile loads for values other CTAs update concurrently
+__device__ __forceinline__ int ld_volatile(const int *p) {
+    return *reinterpret_cast<const volatile int *>(p);
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
+// Software grid barrier for persistent kernels launched cooperatively (all
+// CTAs co-resident).  Sense via a generation counter.
+__device__ __forceinline__ void grid_barrier(unsigned *arrive, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g = *reinterpret_cast<volatile unsigned *>(gen);
+        __threadfence();
+        unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(arrive, 1u) == nb - 1) {
+            *reinterpret_cast<volatile unsigned *>(arrive) = 0;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned *>(gen) == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Workspace control block (device memory, initialised at the start of a call).
+struct Ctrl {
+    // HistoCore lists: F (frontier vertex ids) and S (update segments),
+    // double-buffered counts indexed by round parity (see histocore.cu).
+    unsigned long long nF[2];
+    unsigned long long nS[2];
+    unsigned long long nB;         // init class-B list (warp per vertex)
+    unsigned long long nC;         // init class-C list (CTA per vertex)
+    unsigned long long nX;         // hub fallback list (global bins)
+    unsigned long long rounds;     // HistoCore rounds >= 2 counted on device
+    // PeelOne queue state (a run-wide log of processed (vertex, segment)s)
+    unsigned long long q_head;     // next queue slot to claim
+    unsigned long long q_tail;     // next queue slot to write
+    unsigned long long q_pending;  // pushed but not fully processed entries
+    unsigned long long nAlive[2];  // alive list lengths (ping-pong by level)
+    unsigned long long nProc[2];   // vertices processed per level (parity)
+    unsigned long long levels;     // non-empty levels
+    unsigned long long scans;      // levels scanned
+    int kminb[2];                  // lower bound of the next level (parity)
+    int kmax;
+    int error;                     // device-detected error code (validation)
+    // grid barrier
+    unsigned bar_arrive;
+    unsigned bar_gen;
+    // instrumentation (PICO_F_STATS)
+    unsigned long long st_frontier;
+    unsigned long long st_init_slots;
+    unsigned long long st_arcs;
+    unsigned long long st_guarded;
+    unsigned long long st_bins;
+    unsigned long long st_pushes;
+    unsigned long long st_alive;
+    unsigned long long st_fallback;
+};
+
+// Tunables (degree-class thresholds, bin caps).  PICO_F_TINY_TILES shrinks
+// them so all code paths are exercised by small test graphs.
+struct Tune {
+    int a_max;      // class A (thread per vertex): deg <= a_max (<= 16)
+    int b_max;      // class B (warp per vertex):   a_max < deg <= b_max
+    int c_bins;     // class C (CTA per vertex) shared-memory bin cap
+    int seg;        // arcs per UpdateHisto segment
+};
+
+}  // namespace pico

@@ -1,0 +1,707 @@
+// histocore.cu -- HistoCore (Alg 6) for sm_100a.
+//
+// State in HBM:
+//   core[v]   int32   current estimate h_t(v) (= core_out; P:495 core <- deg)
+//   oldc[v]   int32   estimate before v's latest change (oldcore); during
+//                     init it holds deg(v), the round-0 estimate of every vertex
+//   histo     int32[2m], vertex v owns slots rowptr[v] + b - 1 for bins
+//                     b = 1..deg(v).  Invariant after every
+//                     round: bins b < core[v] count neighbours with
+//                     estimate b, the cap bin core[v] holds cnt(v) = #nbrs with
+//                     estimate >= core[v], bins above are
+//                     stale and never read.
+//   F         int32   frontier list F_t (Theorem 2: cnt < core)
+//   S         int2    UpdateHisto work list: (v, segment) for every changed v,
+//                     one entry per `seg` arcs of v's row (load balance)
+//
+// Round structure (strict two-phase synchronous rounds):
+//   init   = InitHisto fused with round-1 SumHisto: per vertex a
+//            capped histogram of min(deg(u), deg(v)) in registers / shared
+//            memory, its h-index, and only bins 1..h written back (the stale
+//            bins above the cap are never read).  Changed vertices -> S.
+//   loop   { UpdateHisto(S) -> F_{t+1} ; SumHisto(F_{t+1}) -> S }  until F empty
+// UpdateHisto: for v in C_t, u in nbr(v) with core[u] > core[v]:
+//   old = atomicSub(histo[u][min(oldcore[v], core[u])], 1);
+//   atomicAdd(histo[u][core[v]], 1);
+//   push u iff oldcore[v] >= core[u] and old == core[u]   (exactly once,
+//   the cap bin is only ever decremented).
+// SumHisto: walk k = core_old, core_old-1, ...; sum += histo[v][k];
+//   stop at the first k with sum >= k; core[v] = k,
+//   oldcore[v] = core_old, histo[v][k] = sum.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pico {
+
+struct HcArgs {
+    const long long *rp;   // rowptr [n+1]
+    const int *ci;         // colidx [2m]
+    int n;
+    int *core;             // [n]  (core_out)
+    int *oldc;             // [n]
+    int *histo;            // [2m]
+    int *F;                // [n]  frontier list; init: hub fallback list
+    int *BC;               // [n]  init class lists (B from front, C from back)
+    int2 *S;               // [n + 2m/seg + 32] update segments
+    unsigned long long *fsz;  // [fsz_cap] per-round frontier sizes
+    unsigned long long fsz_cap;
+    Ctrl *ctl;
+    Tune tn;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int nseg_of(long long d, int seg) { return (int)((d + seg - 1) / seg); }
+
+// warp-aggregated reservation of nseg segments per lane; writes (v, s) entries
+__device__ __forceinline__ void warp_append_segments(int v, int nseg, int2 *S,
+                                                     unsigned long long *nS) {
+    int incl = warp_incl_scan(nseg);
+    int total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(nS, (unsigned long long)total);
+    base = __shfl_sync(FULL, base, 0);
+    unsigned long long off = base + (unsigned long long)(incl - nseg);
+    for (int s = 0; s < nseg; s++) S[off + s] = make_int2(v, s);
+}
+
+__device__ __forceinline__ void stat_add(unsigned long long *ctr, long long x) {
+    long long s = warp_sum64(x);
+    if (lane_id() == 0 && s) atomicAdd(ctr, (unsigned long long)s);
+}
+
+// ---------------------------------------------------------------------------
+// H0: degrees + classification
+// ---------------------------------------------------------------------------
+__global__ void hc_degree_kernel(HcArgs a) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    long long iters = ((long long)a.n + nthreads - 1) / nthreads;
+    for (long long it = 0; it < iters; it++) {
+        int v = (int)(it * nthreads + blockIdx.x * blockDim.x + threadIdx.x);
+        bool valid = v < a.n;
+        long long d = valid ? a.rp[v + 1] - a.rp[v] : 0;
+        if (valid) {
+            a.oldc[v] = (int)d;  // round-0 estimate of every vertex
+            a.core[v] = (int)d;
+        }
+        bool isB = valid && d > a.tn.a_max && d <= a.tn.b_max;
+        bool isC = valid && d > a.tn.b_max;
+        warp_append(isB, v, a.BC, &a.ctl->nB);
+        // class C grows from the back of the same array
+        unsigned m = __ballot_sync(FULL, isC);
+        if (m) {
+            unsigned long long base = 0;
+            int leader = __ffs(m) - 1;
+            if (lane_id() == leader) base = atomicAdd(&a.ctl->nC, (unsigned long long)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (isC) a.BC[a.n - 1 - (long long)(base + __popc(m & ((1u << lane_id()) - 1)))] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// H1-H3 round 1, class A: one thread per vertex, 1 <= deg <= a_max (<= 16),
+// histogram in registers (compile-time-indexed).
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
+    constexpr int NB = 16;
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    long long iters = ((long long)a.n + nthreads - 1) / nthreads;
+    for (long long it = 0; it < iters; it++) {
+        int v = (int)(it * nthreads + blockIdx.x * blockDim.x + threadIdx.x);
+        bool valid = v < a.n;
+        long long hb = 0;
+        int d = 0;
+        if (valid) {
+            hb = a.rp[v];
+            d = (int)(a.rp[v + 1] - hb);
+        }
+        bool mine = valid && d >= 1 && d <= a.tn.a_max;
+        int nseg = 0, h = 0;
+        if (mine) {
+            int cnt[NB];
+#pragma unroll
+            for (int b = 0; b < NB; b++) cnt[b] = 0;
+            for (int e = 0; e < d; e++) {
+                int u = __ldg(a.ci + hb + e);
+                int x = min(__ldg(a.oldc + u), d);  // min(core[u], core[v])
+#pragma unroll
+                for (int b = 0; b < NB; b++) cnt[b] += (x == b + 1);
+            }
+            int s = 0, hs = 0;
+#pragma unroll
+            for (int b = NB; b >= 1; b--) {
+                if (b <= d && h == 0) {
+                    s += cnt[b - 1];
+                    if (s >= b) { h = b; hs = s; }
+                }
+            }
+#pragma unroll
+            for (int b = 1; b <= NB; b++) {
+                if (b < h) a.histo[hb + b - 1] = cnt[b - 1];
+                else if (b == h) a.histo[hb + b - 1] = hs;
+            }
+            a.core[v] = h;
+            if (h < d) nseg = nseg_of(d, a.tn.seg);
+        }
+        bool changed = nseg > 0;
+        unsigned cm = __ballot_sync(FULL, changed);
+        if (lane_id() == 0 && cm) atomicAdd(&a.ctl->nF[1], (unsigned long long)__popc(cm));
+        warp_append_segments(v, nseg, a.S, &a.ctl->nS[1]);
+        if (STATS) stat_add(&a.ctl->st_init_slots, mine ? h : 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// class B: one warp per vertex, a_max < deg <= b_max, shared-memory bins
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
+    extern __shared__ int sh[];
+    const int wib = threadIdx.x >> 5;
+    const int lane = lane_id();
+    int *bins = sh + wib * (a.tn.b_max + 1);
+    const long long nB = (long long)a.ctl->nB;
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long idx = gw; idx < nB; idx += nw) {
+        int v = a.BC[idx];
+        long long hb = a.rp[v];
+        int d = (int)(a.rp[v + 1] - hb);
+        for (int b = lane; b <= d; b += 32) bins[b] = 0;
+        __syncwarp();
+        for (int e = lane; e < d; e += 32) {
+            int u = __ldg(a.ci + hb + e);
+            int x = min(__ldg(a.oldc + u), d);
+            atomicAdd(&bins[x], 1);
+        }
+        __syncwarp();
+        // descending walk for the h-index (SumHisto on the fresh histogram)
+        int carry = 0, top = d, h = 0, hs = 0;
+        for (;;) {
+            int kk = top - lane;
+            int val = kk >= 1 ? bins[kk] : 0;
+            int incl = warp_incl_scan(val);
+            int s = carry + incl;
+            unsigned m = __ballot_sync(FULL, kk >= 1 && s >= kk);
+            if (m) {
+                int f = __ffs(m) - 1;
+                h = top - f;
+                hs = __shfl_sync(FULL, s, f);
+                break;
+            }
+            carry += __shfl_sync(FULL, incl, 31);
+            top -= 32;
+        }
+        for (int b = 1 + lane; b <= h; b += 32) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
+        __syncwarp();
+        int nseg = (h < d) ? nseg_of(d, a.tn.seg) : 0;
+        if (lane == 0) {
+            a.core[v] = h;
+            if (nseg) atomicAdd(&a.ctl->nF[1], 1ull);
+            if (STATS) atomicAdd(&a.ctl->st_init_slots, (unsigned long long)h);
+        }
+        if (nseg) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&a.ctl->nS[1], (unsigned long long)nseg);
+            base = __shfl_sync(FULL, base, 0);
+            for (int s = lane; s < nseg; s += 32) a.S[base + s] = make_int2(v, s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// class C: one CTA per vertex, shared-memory bins capped at c_bins; vertices
+// whose h-index may exceed the cap go to the global-bin fallback (GLOBAL=true
+// runs the same procedure on the vertex's own 2m-slot region in HBM).
+// ---------------------------------------------------------------------------
+template <bool GLOBAL, bool STATS>
+__device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = lane_id(), wid = tid >> 5, nwarp = nt >> 5;
+    long long hb = a.rp[v];
+    int d = (int)(a.rp[v + 1] - hb);
+    int B = GLOBAL ? d : min(d, a.tn.c_bins);
+    if (GLOBAL) bins = a.histo + hb - 1;  // bin b at slot hb + b - 1
+    for (int b = tid; b <= B; b += nt)
+        if (!GLOBAL || b >= 1) bins[b] = 0;
+    __syncthreads();
+    for (int e = tid; e < d; e += nt) {
+        int u = __ldg(a.ci + hb + e);
+        int x = min(__ldg(a.oldc + u), B);
+        atomicAdd(&bins[x], 1);
+    }
+    __syncthreads();
+    // block-wide descending search: h = max b in 1..B with sum_{j>=b} bins[j] >= b
+    int c = (B + nt - 1) / nt;
+    int hiT = B - tid * c;              // this thread's chunk, descending
+    int loT = max(1, B - (tid + 1) * c + 1);
+    int tsum = 0;
+    for (int b = hiT; b >= loT; b--) tsum += bins[b];
+    // block exclusive scan of tsum in thread order
+    int incl = warp_incl_scan(tsum);
+    if (lane == 31) red[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int x = lane < nwarp ? red[lane] : 0;
+        int xi = warp_incl_scan(x);
+        if (lane < nwarp) red[lane] = xi - x;  // exclusive warp offsets
+    }
+    __syncthreads();
+    int s = red[wid] + incl - tsum;
+    int cand = 0, cs = 0;
+    for (int b = hiT; b >= loT; b--) {
+        s += bins[b];
+        if (s >= b) { cand = b; cs = s; break; }
+    }
+    __syncthreads();
+    if (tid == 0) { red[32] = 0; red[33] = 0; }
+    __syncthreads();
+    if (cand) atomicMax(&red[32], cand);
+    __syncthreads();
+    int h = red[32];
+    if (cand == h && cand) red[33] = cs;
+    __syncthreads();
+    int hs = red[33];
+    if (!GLOBAL && h == B && d > B) {
+        // the cap may hide a larger h-index: redo with global bins
+        if (tid == 0) {
+            unsigned long long i = atomicAdd(&a.ctl->nX, 1ull);
+            a.F[i] = v;
+        }
+        __syncthreads();
+        return;
+    }
+    if (GLOBAL) {
+        if (tid == 0) a.histo[hb + h - 1] = hs;  // bins 1..h-1 already exact
+    } else {
+        for (int b = 1 + tid; b <= h; b += nt) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
+    }
+    int nseg = (h < d) ? nseg_of(d, a.tn.seg) : 0;
+    if (tid == 0) {
+        a.core[v] = h;
+        if (nseg) {
+            atomicAdd(&a.ctl->nF[1], 1ull);
+            red[34] = (int)atomicAdd(&a.ctl->nS[1], (unsigned long long)nseg);
+        }
+        if (STATS) {
+            atomicAdd(&a.ctl->st_init_slots, (unsigned long long)(GLOBAL ? d : h));
+            if (GLOBAL) atomicAdd(&a.ctl->st_fallback, 1ull);
+        }
+    }
+    __syncthreads();
+    if (nseg) {
+        unsigned long long base = (unsigned)red[34];
+        for (int s2 = tid; s2 < nseg; s2 += nt) a.S[base + s2] = make_int2(v, s2);
+    }
+    __syncthreads();
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(512) hc_init_cta_kernel(HcArgs a) {
+    extern __shared__ int bins[];
+    __shared__ int red[40];
+    const long long nC = (long long)a.ctl->nC;
+    for (long long idx = blockIdx.x; idx < nC; idx += gridDim.x) {
+        int v = a.BC[a.n - 1 - idx];
+        cta_init_vertex<false, STATS>(a, v, bins, red);
+    }
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
+    __shared__ int red[40];
+    const long long nX = (long long)a.ctl->nX;
+    for (long long idx = blockIdx.x; idx < nX; idx += gridDim.x) {
+        int v = a.F[idx];
+        cta_init_vertex<true, STATS>(a, v, nullptr, red);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// UpdateHisto phase of round t: segments of C_t (count nS[t&1]) -> F_{t+1}
+// (count nF[(t+1)&1]).  Warp-centric load balancing: a warp takes 32 segments,
+// scans their lengths, and walks the concatenated arcs 32 at a time, each
+// lane locating its segment by a 5-step shuffle binary search.
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__device__ void update_phase(const HcArgs &a, int t, long long gwarp, long long nwarps) {
+    const int lane = lane_id();
+    const long long ns = (long long)ld_volatile(&a.ctl->nS[t & 1]);
+    unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
+    long long st_arcs = 0, st_guard = 0, st_push = 0;
+    for (long long base = gwarp * 32; base < ns; base += nwarps * 32) {
+        long long i = base + lane;
+        long long b = 0;
+        int len = 0, cv = 0, ov = 0;
+        if (i < ns) {
+            int2 sg = __ldcg(a.S + i);
+            long long r0 = a.rp[sg.x], r1 = a.rp[sg.x + 1];
+            b = r0 + (long long)sg.y * a.tn.seg;
+            len = (int)min((long long)a.tn.seg, r1 - b);
+            cv = __ldcg(a.core + sg.x);
+            ov = __ldcg(a.oldc + sg.x);
+        }
+        int incl = warp_incl_scan(len);
+        int excl = incl - len;
+        int total = __shfl_sync(FULL, incl, 31);
+        for (int j0 = 0; j0 < total; j0 += 32) {
+            int j = j0 + lane;
+            // owner = max lane with excl <= j
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                int cand = lo + step;
+                int ex = __shfl_sync(FULL, excl, cand & 31);
+                if (cand < 32 && ex <= j) lo = cand;
+            }
+            long long eb = __shfl_sync(FULL, b, lo);
+            int ex = __shfl_sync(FULL, excl, lo);
+            int cvo = __shfl_sync(FULL, cv, lo);
+            int ovo = __shfl_sync(FULL, ov, lo);
+            bool push = false;
+            int u = 0;
+            if (j < total) {
+                u = __ldg(a.ci + eb + (j - ex));
+                int cu = __ldcg(a.core + u);
+                if (STATS) st_arcs++;
+                if (cu > cvo) {  // N1/N3 neighbour
+                    long long hbu = a.rp[u] - 1;
+                    if (ovo >= cu) {
+                        int old = atomicSub(a.histo + hbu + cu, 1);  // cap bin
+                        push = (old == cu);
+                    } else {
+                        atomicSub(a.histo + hbu + ovo, 1);
+                    }
+                    atomicAdd(a.histo + hbu + cvo, 1);
+                    if (STATS) st_guard++;
+                }
+            }
+            warp_append(push, u, a.F, nF);
+            if (STATS) st_push += push;
+        }
+    }
+    if (STATS) {
+        stat_add(&a.ctl->st_arcs, st_arcs);
+        stat_add(&a.ctl->st_guarded, st_guard);
+        stat_add(&a.ctl->st_pushes, st_push);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SumHisto phase of round t: F_t (count nF[t&1]) -> core/oldcore/cap bin and
+// segments of C_t (count nS[t&1]).  Thread per vertex for the first 32 bins
+// of the descending walk, then warp-cooperative 32-bin chunks for long walks.
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long nthreads) {
+    const int lane = lane_id();
+    const long long nf = (long long)ld_volatile(&a.ctl->nF[t & 1]);
+    unsigned long long *nS = &a.ctl->nS[t & 1];
+    long long iters = (nf + nthreads - 1) / nthreads;
+    long long st_bins = 0;
+    for (long long it = 0; it < iters; it++) {
+        long long i = it * nthreads + gthread;
+        bool valid = i < nf;
+        int v = 0, cold = 0, k = 0, sum = 0;
+        long long hb = 0, d = 0;
+        bool done = true;
+        if (valid) {
+            v = __ldcg(a.F + i);
+            cold = __ldcg(a.core + v);
+            hb = a.rp[v] - 1;  // bin b at hb + b
+            d = a.rp[v + 1] - hb - 1;
+            k = cold;
+            done = false;
+            for (int stp = 0; stp < 32; stp++) {
+                sum += __ldcg(a.histo + hb + k);
+                if (STATS) st_bins++;
+                if (sum >= k) { done = true; break; }
+                k--;
+            }
+        }
+        unsigned m = __ballot_sync(FULL, !done);
+        while (m) {
+            int L = __ffs(m) - 1;
+            m &= m - 1;
+            long long hbL = __shfl_sync(FULL, hb, L);
+            int kL = __shfl_sync(FULL, k, L);
+            int sL = __shfl_sync(FULL, sum, L);
+            int rk = 0, rs = 0;
+            for (;;) {
+                int kk = kL - lane;
+                int val = kk >= 1 ? __ldcg(a.histo + hbL + kk) : 0;
+                int incl = warp_incl_scan(val);
+                int s = sL + incl;
+                unsigned mm = __ballot_sync(FULL, kk >= 1 && s >= kk);
+                if (STATS) st_bins += (kk >= 1) ? 1 : 0;
+                if (mm) {
+                    int f = __ffs(mm) - 1;
+                    rk = kL - f;
+                    rs = __shfl_sync(FULL, s, f);
+                    break;
+                }
+                sL += __shfl_sync(FULL, incl, 31);
+                kL -= 32;
+            }
+            if (lane == L) { k = rk; sum = rs; }
+        }
+        int nseg = 0;
+        if (valid) {
+            a.core[v] = k;
+            a.oldc[v] = cold;
+            a.histo[hb + k] = sum;  // cap bin := cnt
+            nseg = nseg_of(d, a.tn.seg);
+        }
+        warp_append_segments(v, nseg, a.S, nS);
+    }
+    if (STATS) stat_add(&a.ctl->st_bins, st_bins);
+}
+
+// ---------------------------------------------------------------------------
+// persistent cooperative kernel: all rounds t >= 1 with grid barriers
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__global__ void __launch_bounds__(512) hc_rounds_kernel(HcArgs a) {
+    const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    const long long gwarp = gthread >> 5, nwarps = nthreads >> 5;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    if (ld_volatile(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
+    for (int t = 1;; t++) {
+        if (leader) a.ctl->nS[(t + 1) & 1] = 0;
+        update_phase<STATS>(a, t, gwarp, nwarps);
+        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        unsigned long long nf = ld_volatile(&a.ctl->nF[(t + 1) & 1]);
+        if (nf == 0) break;
+        if (leader) {
+            a.ctl->nF[t & 1] = 0;
+            a.ctl->rounds++;
+            if ((unsigned long long)t < a.fsz_cap) a.fsz[t] = nf;
+            if (STATS) a.ctl->st_frontier += nf;
+        }
+        sum_phase<STATS>(a, t + 1, gthread, nthreads);
+        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+    }
+}
+
+// host-loop variants (PICO_F_HOST_LOOP): one launch per phase
+template <bool STATS>
+__global__ void __launch_bounds__(512) hc_update_kernel(HcArgs a, int t) {
+    const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->nS[(t + 1) & 1] = 0;
+    update_phase<STATS>(a, t, gthread >> 5, nthreads >> 5);
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(512) hc_sum_kernel(HcArgs a, int t) {
+    const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->nF[(t + 1) & 1] = 0;
+        a.ctl->rounds++;
+    }
+    sum_phase<STATS>(a, t, gthread, nthreads);
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+Tune hc_tune(uint32_t flags) {
+    Tune t;
+    if (flags & PICO_F_TINY_TILES) {
+        t.a_max = 4; t.b_max = 12; t.c_bins = 16; t.seg = 4;
+    } else {
+        t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = 256;
+    }
+    return t;
+}
+
+size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags) {
+    Tune tn = hc_tune(flags);
+    size_t b = 0;
+    b += align256(sizeof(Ctrl));
+    b += align256(sizeof(unsigned long long) * kFszCap);
+    b += align256(sizeof(int) * (size_t)arcs);             // histo
+    b += align256(sizeof(int) * (size_t)n) * 3;           // oldc, F, BC
+    b += align256(sizeof(int2) * (size_t)(n + arcs / tn.seg + 64));  // S
+    return b;
+}
+
+struct Timer {
+    cudaStream_t s;
+    bool on;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    void start(int slot) {
+        if (!on) return;
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        ev.push_back({slot, {a, b}});
+    }
+    void stop() {
+        if (!on) return;
+        cudaEventRecord(ev.back().second.second, s);
+    }
+    void collect(pico_stats_t *st) {
+        for (auto &e : ev) {
+            float ms = 0;
+            cudaEventSynchronize(e.second.second);
+            cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+            if (st) {
+                st->kernel_ms[e.first] += ms;
+                st->kernel_launches[e.first] += 1;
+            }
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+        ev.clear();
+    }
+};
+
+template <bool STATS>
+static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, long long arcs,
+                            int *core, cudaStream_t s, uint32_t flags, void *ws,
+                            pico_stats_t *st, const DevInfo &dev) {
+    HcArgs a;
+    Tune tn = hc_tune(flags);
+    char *p = (char *)ws;
+    a.ctl = (Ctrl *)p; p += align256(sizeof(Ctrl));
+    a.fsz = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * kFszCap);
+    a.fsz_cap = kFszCap;
+    a.histo = (int *)p; p += align256(sizeof(int) * (size_t)arcs);
+    a.oldc = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.F = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.BC = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.S = (int2 *)p;
+    a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core; a.tn = tn;
+
+    Timer tm{s, (flags & PICO_F_TIMING) != 0, {}};
+    cudaError_t err;
+    if ((err = cudaMemsetAsync(a.ctl, 0, sizeof(Ctrl), s))) return err;
+
+    const int sms = dev.sms;
+    // H0
+    tm.start(PICO_K_DEGREE);
+    {
+        int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 16);
+        hc_degree_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+    }
+    tm.stop();
+    // H1-H3 (round 1)
+    tm.start(PICO_K_INIT);
+    {
+        int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
+        hc_init_small_kernel<STATS><<<std::max(blocks, 1), 256, 0, s>>>(a);
+        size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
+        cudaFuncSetAttribute(hc_init_warp_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smB);
+        hc_init_warp_kernel<STATS><<<sms * 4, 256, smB, s>>>(a);
+        size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
+        cudaFuncSetAttribute(hc_init_cta_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smC);
+        hc_init_cta_kernel<STATS><<<sms, 512, smC, s>>>(a);
+        hc_init_fallback_kernel<STATS><<<sms, 512, 0, s>>>(a);
+    }
+    tm.stop();
+    if ((err = cudaGetLastError())) return err;
+
+    unsigned long long c1 = 0;
+    if ((err = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return err;
+    if ((err = cudaStreamSynchronize(s))) return err;
+    // F_1 = C_1 (Theorem 2), recorded at fsz[0]
+    unsigned long long rounds = c1 ? 1 : 0;
+    std::vector<unsigned long long> hsz;
+    if (c1) hsz.push_back(c1);
+    // counters as the rounds expect them: nF[1] held |C_1|, F list empty
+    if ((err = cudaMemsetAsync(&a.ctl->nF[1], 0, sizeof(unsigned long long), s))) return err;
+
+    if (c1) {
+        if (flags & PICO_F_HOST_LOOP) {
+            int blocks = sms * 4;
+            for (int t = 1;; t++) {
+                tm.start(PICO_K_UPDATE);
+                hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t);
+                tm.stop();
+                unsigned long long nf = 0;
+                if ((err = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf),
+                                           cudaMemcpyDeviceToHost, s)))
+                    return err;
+                if ((err = cudaStreamSynchronize(s))) return err;
+                if (nf == 0) break;
+                rounds++;
+                hsz.push_back(nf);
+                int sb = (int)std::min<long long>(((long long)nf + 511) / 512, (long long)sms * 4);
+                tm.start(PICO_K_SUM);
+                hc_sum_kernel<STATS><<<std::max(sb, 1), 512, 0, s>>>(a, t + 1);
+                tm.stop();
+            }
+            if (STATS) {
+                unsigned long long tot = 0;
+                for (auto x : hsz) tot += x;
+                // frontier_total filled below from hsz
+                (void)tot;
+            }
+        } else {
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hc_rounds_kernel<STATS>, 512, 0);
+            int per = std::max(1, std::min(occ, 2));
+            int blocks = sms * per;
+            void *args[] = {&a};
+            tm.start(PICO_K_ROUNDS);
+            err = cudaLaunchCooperativeKernel((const void *)hc_rounds_kernel<STATS>, blocks, 512, args, 0, s);
+            tm.stop();
+            if (err) return err;
+            unsigned long long devrounds = 0;
+            if ((err = cudaMemcpyAsync(&devrounds, &a.ctl->rounds, sizeof(devrounds),
+                                       cudaMemcpyDeviceToHost, s)))
+                return err;
+            std::vector<unsigned long long> dsz(std::min<unsigned long long>(devrounds + 1, kFszCap), 0);
+            if (!dsz.empty() &&
+                (err = cudaMemcpyAsync(dsz.data(), a.fsz, sizeof(unsigned long long) * dsz.size(),
+                                       cudaMemcpyDeviceToHost, s)))
+                return err;
+            if ((err = cudaStreamSynchronize(s))) return err;
+            rounds += devrounds;
+            for (unsigned long long t = 1; t <= devrounds && t < kFszCap; t++) hsz.push_back(dsz[t]);
+        }
+    }
+    if ((err = cudaGetLastError())) return err;
+    if (st) {
+        st->rounds = (int64_t)rounds;
+        if (st->frontier_sizes)
+            for (size_t i = 0; i < hsz.size() && (int64_t)i < st->frontier_sizes_cap; i++)
+                st->frontier_sizes[i] = (int64_t)hsz[i];
+        if (STATS) {
+            Ctrl h;
+            if ((err = cudaMemcpyAsync(&h, a.ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s))) return err;
+            if ((err = cudaStreamSynchronize(s))) return err;
+            unsigned long long tot = 0;
+            for (auto x : hsz) tot += x;
+            st->frontier_total = (int64_t)tot;
+            st->init_slots_written = (int64_t)h.st_init_slots;
+            st->arcs_scanned = (int64_t)h.st_arcs;
+            st->guarded_arcs = (int64_t)h.st_guarded;
+            st->bins_read = (int64_t)h.st_bins;
+            st->pushes = (int64_t)h.st_pushes;
+            st->hub_fallbacks = (int64_t)h.st_fallback;
+        }
+    }
+    tm.collect(st);
+    return cudaSuccess;
+}
+
+cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
+                   cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev) {
+    if (flags & PICO_F_STATS) return hc_run_t<true>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
+    return hc_run_t<false>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
+}
+
+}  // namespace pico

@@ -1,0 +1,33 @@
+// kernels.h -- internal host-side interface between the C ABI (capi.cu) and
+// the algorithm drivers (histocore.cu, peelone.cu, shard.cu).
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+
+#include "pico.h"
+
+namespace pico {
+
+constexpr unsigned long long kFszCap = 1ull << 16;  // per-round sizes recorded
+
+struct DevInfo {
+    int device;
+    int sms;
+    int coop;  // cooperative launch supported
+};
+
+size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags);
+cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
+                   cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);
+
+size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags);
+cudaError_t po_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
+                   cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);
+
+size_t validate_workspace_bytes();
+cudaError_t validate_run(const long long *rp, const int *ci, long long n, long long arcs,
+                         cudaStream_t s, void *ws, int *bad);
+
+}  // namespace pico

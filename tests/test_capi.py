@@ -1,0 +1,153 @@
+"""T9: the C ABI of include/pico.h.  CPU tests load the library and call only
+host-side paths (no compute); GPU tests exercise status codes end to end."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2402_15253_b200 as pico
+from paper_2402_15253_b200 import _lib
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2402_15253_b200 import build
+    build.build()
+    return pico.load()
+
+
+def test_exports_every_header_symbol(lib):
+    names = pico.header_functions()
+    assert "pico_coreness" in names and "pico_coreness_ex" in names and "pico_coreness_host" in names
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_status_strings_and_version(lib):
+    for code, name in _lib.STATUS.items():
+        assert lib.pico_status_string(code).decode() == name
+    assert lib.pico_status_string(99).decode() == "PICO_UNKNOWN"
+    assert lib.pico_version() >= 100
+
+
+def test_workspace_bytes_monotone(lib):
+    a = pico.workspace_bytes(1000, 5000, "histocore")
+    b = pico.workspace_bytes(1000, 50000, "histocore")
+    c = pico.workspace_bytes(1000, 5000, "peelone")
+    assert 0 < a < b and c > 0
+    # histogram = 2m int32 slots dominate HistoCore's workspace
+    assert b - a >= 4 * 2 * 45000
+    assert pico.workspace_bytes(0, 0, "histocore") == 256
+
+
+def test_host_side_argument_errors(lib):
+    """Rejected before any device work, so safe without a GPU."""
+    rp = np.zeros(3, dtype=np.int64)
+    ci = np.zeros(2, dtype=np.int32)
+    core = np.zeros(2, dtype=np.int32)
+    f = lib.pico_coreness_ex
+    P = rp.ctypes.data
+    assert f(P, ci.ctypes.data, -1, 0, 0, core.ctypes.data, None, 0, None, 0, None) == 1
+    assert f(P, ci.ctypes.data, 2, -1, 0, core.ctypes.data, None, 0, None, 0, None) == 1
+    assert f(P, ci.ctypes.data, 2, 1, 7, core.ctypes.data, None, 0, None, 0, None) == 1
+    assert b"unknown algo" in lib.pico_last_error()
+    assert f(None, ci.ctypes.data, 2, 1, 0, core.ctypes.data, None, 0, None, 0, None) == 1
+    assert f(P, None, 2, 1, 0, core.ctypes.data, None, 0, None, 0, None) == 1
+    assert f(P, ci.ctypes.data, 2, 1, 0, None, None, 0, None, 0, None) == 1
+    assert f(P, ci.ctypes.data, 1 << 31, 1, 0, core.ctypes.data, None, 0, None, 0, None) == 2
+    # n == 0 is a no-op returning PICO_OK
+    assert f(P, ci.ctypes.data, 0, 0, 0, None, None, 0, None, 0, None) == 0
+    assert lib.pico_coreness(P, ci.ctypes.data, 0, 0, 1, None, None) == 0
+    # too-small caller workspace
+    assert f(P, ci.ctypes.data, 2, 1, 0, core.ctypes.data, None, 0, 1024, 16, None) == 1
+    assert b"workspace too small" in lib.pico_last_error()
+    # host entry point shares the checks
+    assert lib.pico_coreness_host(P, ci.ctypes.data, -5, 1, 0, core.ctypes.data, None, 0, None) == 1
+    assert lib.pico_coreness_host(P, ci.ctypes.data, 0, 0, 0, None, None, 0, None) == 0
+
+
+def test_stats_struct_layout():
+    # pico_stats_t: 12 int64 + double[8] + int64[8] + pointer + int64
+    assert ctypes.sizeof(_lib.Stats) == 12 * 8 + 8 * 8 + 8 * 8 + 8 + 8
+
+
+def test_python_api_refuses_cpu_tensors(lib):
+    import torch
+    rp = torch.zeros(3, dtype=torch.int64)
+    ci = torch.zeros(2, dtype=torch.int32)
+    with pytest.raises(ValueError, match="CUDA"):
+        pico.coreness(rp, ci)
+
+
+# ---------------------------------------------------------------- GPU
+def _dev():
+    import torch
+    return torch.device("cuda:0")
+
+
+@pytest.mark.gpu
+def test_validate_rejects_malformed():
+    import torch
+    dev = _dev()
+
+    def run(rp, ci, n):
+        return pico.coreness(torch.tensor(rp, dtype=torch.int64, device=dev),
+                             torch.tensor(ci, dtype=torch.int32, device=dev), flags=pico.F_VALIDATE)
+
+    # good: path 0-1-2
+    assert run([0, 1, 3, 4], [1, 0, 2, 1], 3).cpu().tolist() == [1, 1, 1]
+    cases = {
+        "self-loop": ([0, 2, 3, 4], [0, 1, 0, 1], 3),  # bad: 0-0 loop (also asym counts)
+        "duplicate": ([0, 2, 4], [1, 1, 0, 0], 2),
+        "asymmetric": ([0, 1, 1, 2], [1, 0], 3),
+        "range": ([0, 1, 2], [5, 0], 2),
+        "rowptr": ([0, 3, 2], [1, 0], 2),
+    }
+    for name, (rp, ci, n) in cases.items():
+        if len(ci) % 2:
+            continue
+        with pytest.raises(pico.PicoError) as ei:
+            run(rp, ci, n)
+        assert ei.value.status == 6, name
+
+
+@pytest.mark.gpu
+def test_inputs_untouched_and_workspace():
+    import torch
+    import synth
+    dev = _dev()
+    rp, ci = synth.CONFIGS["R12"].build(device=dev)
+    rp0, ci0 = rp.clone(), ci.clone()
+    for algo in ("histocore", "peelone"):
+        need = pico.workspace_bytes(rp.numel() - 1, ci.numel() // 2, algo)
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        a = pico.coreness(rp, ci, algo=algo, workspace=ws)
+        b = pico.coreness(rp, ci, algo=algo)
+        assert torch.equal(a, b)
+        small = torch.empty(need // 2, dtype=torch.uint8, device=dev)
+        with pytest.raises(pico.PicoError) as ei:
+            pico.coreness(rp, ci, algo=algo, workspace=small)
+        assert ei.value.status == 1
+    assert torch.equal(rp, rp0) and torch.equal(ci, ci0)
+
+
+@pytest.mark.gpu
+def test_edgeless_and_isolated():
+    import torch
+    dev = _dev()
+    rp = torch.zeros(6, dtype=torch.int64, device=dev)
+    ci = torch.zeros(0, dtype=torch.int32, device=dev)
+    for algo in ("histocore", "peelone"):
+        assert pico.coreness(rp, ci, algo=algo).cpu().tolist() == [0] * 5
+
+
+@pytest.mark.gpu
+def test_host_entry_point_matches_device():
+    import synth
+    import oracle
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    ref = oracle.bz(rp, ci)
+    for algo in ("histocore", "peelone"):
+        st = pico.Stats()
+        core = pico.coreness_host(rp, ci, algo=algo, stats=st)
+        assert np.array_equal(core, ref)

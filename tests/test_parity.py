@@ -1,0 +1,181 @@
+"""T2/T3: GPU parity.  The CUDA path (through the C ABI) against the CPU
+oracle, element by element (bit-exact: coreness is integer and unique,
+SURVEY 8(c)), plus iteration counts: HistoCore's l2 and every |F_t| equal the
+synchronous Index2core sweeps; PeelOne's non-empty levels equal the number of
+distinct nonzero coreness values and its k_max the maximum."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ("histocore", "peelone")
+
+
+def _pico():
+    import paper_2402_15253_b200 as pico
+    return pico
+
+
+def _variants(algo):
+    pico = _pico()
+    base = [0, pico.F_HOST_LOOP, pico.F_TINY_TILES, pico.F_TINY_TILES | pico.F_HOST_LOOP, pico.F_STATS]
+    if algo == "peelone":
+        base += [pico.F_CLAMP_SUB, pico.F_CLAMP_SUB | pico.F_HOST_LOOP, pico.F_CLAMP_SUB | pico.F_TINY_TILES]
+    return base
+
+
+def _run(rp_np, ci_np, algo, flags=0, fs_cap=1 << 16):
+    import torch
+    pico = _pico()
+    dev = torch.device("cuda:0")
+    rp = torch.from_numpy(rp_np).to(dev)
+    ci = torch.from_numpy(ci_np).to(dev)
+    st = pico.Stats()
+    fs = np.zeros(fs_cap, dtype=np.int64)
+    core = pico.coreness(rp, ci, algo=algo, flags=flags, stats=st, frontier_sizes=fs)
+    torch.cuda.synchronize()
+    return core.cpu().numpy(), st, fs
+
+
+def _check(rp, ci, algo, flags, ref=None, jac=None):
+    if ref is None:
+        ref = oracle.bz(rp, ci)
+    core, st, fs = _run(rp, ci, algo, flags)
+    if not np.array_equal(core, ref):
+        bad = np.flatnonzero(core != ref)
+        raise AssertionError(f"{algo} flags={flags}: {bad.size} mismatches, first v={bad[0]} "
+                             f"gpu={core[bad[0]]} ref={ref[bad[0]]}")
+    if algo == "histocore":
+        if jac is None:
+            jac = oracle.jacobi_rounds(rp, ci)
+        _, l2, sizes = jac
+        assert st.rounds == l2, (st.rounds, l2)
+        assert list(fs[:l2]) == sizes
+    else:
+        nz = ref[ref > 0]
+        assert st.levels == len(np.unique(nz))
+        assert st.kmax == (int(nz.max()) if nz.size else 0)
+        # vertices processed per level sum to the non-isolated count
+        assert int(fs[:st.levels].sum()) == nz.size
+    return st
+
+
+# ------------------------------------------------------------------ fixtures
+def _fixture_graphs():
+    from conftest import parse_small_fixtures, parse_g1, csr_np
+    out = []
+    g = parse_g1()
+    edges = [tuple(int(x) for x in p.split("-")) for p in g["edges"].split()]
+    out.append(("G1", csr_np(6, edges)))
+    for fx in parse_small_fixtures():
+        out.append((fx["name"], csr_np(fx["n"], fx["edges"])))
+    out.append(("K20", csr_np(20, [(i, j) for i in range(20) for j in range(i + 1, 20)])))
+    out.append(("K5_7", csr_np(12, [(i, 5 + j) for i in range(5) for j in range(7)])))
+    out.append(("star200", csr_np(201, [(0, i) for i in range(1, 201)])))
+    out.append(("single", csr_np(2, [(0, 1)])))
+    return out
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("name,g", _fixture_graphs(), ids=[x[0] for x in _fixture_graphs()])
+def test_fixtures(algo, name, g):
+    rp, ci = g
+    for fl in _variants(algo):
+        _check(rp, ci, algo, fl)
+
+
+def test_g1_paper_values():
+    """G1: coreness [1,1,2,2,2,2]; HistoCore l2 = 1; PO-dyn 2
+    levels = k_max; Fig 6 path: v5 5 -> 2 with no slot writes."""
+    from conftest import parse_g1, csr_np
+    g = parse_g1()
+    edges = [tuple(int(x) for x in p.split("-")) for p in g["edges"].split()]
+    rp, ci = csr_np(6, edges)
+    core, st, _ = _run(rp, ci, "histocore", _pico().F_STATS)
+    assert core.tolist() == [1, 1, 2, 2, 2, 2] and st.rounds == 1
+    assert st.guarded_arcs == 0  # UpdateHisto: no neighbour has core > 2
+    core, st, _ = _run(rp, ci, "peelone", _pico().F_STATS)
+    assert core.tolist() == [1, 1, 2, 2, 2, 2] and st.levels == 2 and st.kmax == 2
+
+
+# ------------------------------------------------------------------ corpus
+def _corpus():
+    out = []
+    for i, (n, p) in enumerate([(30, 0.2), (100, 0.02), (100, 0.05), (150, 0.2), (200, 0.8),
+                                (200, 0.05), (64, 0.5), (180, 0.1)]):
+        out.append((f"er{i}", synth.to_numpy(*synth.erdos_renyi(n, p, seed=1000 + i))))
+    for i, (n, e) in enumerate([(1000, 2.2), (3000, 2.5), (5000, 2.1)]):
+        out.append((f"cl{i}", synth.to_numpy(*synth.chung_lu(n, 10.0, e, seed=2000 + i))))
+    out.append(("R12", synth.to_numpy(*synth.CONFIGS["R12"].build())))
+    out.append(("R14", synth.to_numpy(*synth.CONFIGS["R14"].build())))
+    return out
+
+
+_CORPUS = None
+
+
+def corpus():
+    global _CORPUS
+    if _CORPUS is None:
+        _CORPUS = _corpus()
+    return _CORPUS
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_corpus_all_variants(algo):
+    for name, (rp, ci) in corpus():
+        ref = oracle.bz(rp, ci)
+        jac = oracle.jacobi_rounds(rp, ci) if algo == "histocore" else None
+        for fl in _variants(algo):
+            _check(rp, ci, algo, fl, ref, jac)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_schedule_robustness_repeat(algo):
+    """5 repetitions give the identical result (atomics interleave
+    differently every run)."""
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R14"].build())
+    ref = oracle.bz(rp, ci)
+    jac = oracle.jacobi_rounds(rp, ci)
+    for _ in range(5):
+        _check(rp, ci, algo, 0, ref, jac if algo == "histocore" else None)
+
+
+def test_er_property_corpus_200():
+    """S:463 corpus: 200 ER graphs n <= 200, p in {0.02, 0.05, 0.2, 0.8}."""
+    ps = [0.02, 0.05, 0.2, 0.8]
+    for i in range(200):
+        n = 20 + (i * 37) % 181
+        rp, ci = synth.to_numpy(*synth.erdos_renyi(n, ps[i % 4], seed=5000 + i))
+        ref = oracle.bz(rp, ci)
+        for algo in ALGOS:
+            core, _, _ = _run(rp, ci, algo)
+            assert np.array_equal(core, ref), (i, algo)
+
+
+# ------------------------------------------------------------ larger graphs
+def test_c1_rmat16_full():
+    """configs[0]: RMAT scale-16 ef16 vs the oracle, both algorithms, with the
+    invariants of the north star (core <= deg, k-core definition)."""
+    rp, ci = synth.to_numpy(*synth.CONFIGS["C1"].build())
+    ref = oracle.bz(rp, ci)
+    jac = oracle.jacobi_rounds(rp, ci)
+    for algo in ALGOS:
+        for fl in (0, _pico().F_HOST_LOOP, _pico().F_STATS):
+            _check(rp, ci, algo, fl, ref, jac)
+    assert oracle.kcore_check(rp, ci, ref)
+
+
+def test_gpu_generator_matches_cpu():
+    """The shared generator is bit-identical on CPU and GPU (inputs of the
+    oracle and of the CUDA path are the same graph)."""
+    import torch
+    a = synth.CONFIGS["R14"].build(device="cpu")
+    b = synth.CONFIGS["R14"].build(device=torch.device("cuda:0"))
+    assert torch.equal(a[0], b[0].cpu()) and torch.equal(a[1], b[1].cpu())
+    c = synth.erdos_renyi(300, 0.05, seed=9, device="cpu")
+    d = synth.erdos_renyi(300, 0.05, seed=9, device=torch.device("cuda:0"))
+    assert torch.equal(c[1], d[1].cpu())
