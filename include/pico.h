@@ -117,6 +117,10 @@ typedef struct {
     int64_t pushes;             /* vertices pushed into a next frontier/queue  */
     int64_t alive_scanned;      /* PeelOne: sum over levels of |alive list|    */
     int64_t hub_fallbacks;      /* vertices that needed the global-bin path    */
+    int64_t segments;           /* HistoCore: UpdateHisto work items (v, seg)  */
+                                /* produced; PeelOne: queue entries processed  */
+    int64_t segments_init;      /* HistoCore: of which produced by init        */
+    int64_t kernel_count;       /* kernels this library launched in the call   */
     /* per-kernel device time (PICO_F_TIMING) */
     double kernel_ms[PICO_K_COUNT];
     int64_t kernel_launches[PICO_K_COUNT];

@@ -47,6 +47,9 @@ class Stats(ctypes.Structure):
         ("pushes", ctypes.c_int64),
         ("alive_scanned", ctypes.c_int64),
         ("hub_fallbacks", ctypes.c_int64),
+        ("segments", ctypes.c_int64),
+        ("segments_init", ctypes.c_int64),
+        ("kernel_count", ctypes.c_int64),
         ("kernel_ms", ctypes.c_double * 8),
         ("kernel_launches", ctypes.c_int64 * 8),
         ("frontier_sizes", ctypes.POINTER(ctypes.c_int64)),
@@ -54,7 +57,7 @@ class Stats(ctypes.Structure):
     ]
 
     def to_dict(self) -> dict:
-        d = {k: int(getattr(self, k)) for k, _ in self._fields_[:12]}
+        d = {k: int(getattr(self, k)) for k, _ in self._fields_[:15]}
         d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(8) if self.kernel_launches[i]}
         d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(8) if self.kernel_launches[i]}
         return d

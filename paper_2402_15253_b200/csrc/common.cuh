@@ -66,6 +66,11 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
     return *reinterpret_cast<const volatile unsigned long long *>(p);
 }
 
+// fire-and-forget global reduction (REDG), relaxed, device scope
+__device__ __forceinline__ void red_add(int *p, int v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Software grid barrier for persistent kernels launched cooperatively (all
 // CTAs co-resident).  Sense via a generation counter.
 __device__ __forceinline__ void grid_barrier(unsigned *arrive, unsigned *gen) {
@@ -96,10 +101,13 @@ struct Ctrl {
     unsigned long long nC;         // init class-C list (CTA per vertex)
     unsigned long long nX;         // hub fallback list (global bins)
     unsigned long long rounds;     // HistoCore rounds >= 2 counted on device
-    // PeelOne queue state (a run-wide log of processed (vertex, segment)s)
-    unsigned long long q_head;     // next queue slot to claim
-    unsigned long long q_tail;     // next queue slot to write
-    unsigned long long q_pending;  // pushed but not fully processed entries
+    unsigned long long wc[2];      // UpdateHisto batch claim counters (parity)
+    // PeelOne queue state (a run-wide log of processed (vertex, segment)s);
+    // each hot word on its own 128-byte line (polling vs. atomics)
+    alignas(128) unsigned long long q_head;     // next queue slot to claim
+    alignas(128) unsigned long long q_tail;     // next queue slot to write
+    alignas(128) unsigned long long q_pending;  // pushed, not fully processed
+    alignas(128) unsigned long long q_pad;
     unsigned long long nAlive[2];  // alive list lengths (ping-pong by level)
     unsigned long long nProc[2];   // vertices processed per level (parity)
     unsigned long long levels;     // non-empty levels
@@ -107,9 +115,9 @@ struct Ctrl {
     int kminb[2];                  // lower bound of the next level (parity)
     int kmax;
     int error;                     // device-detected error code (validation)
-    // grid barrier
-    unsigned bar_arrive;
-    unsigned bar_gen;
+    // grid barrier (own lines)
+    alignas(128) unsigned bar_arrive;
+    alignas(128) unsigned bar_gen;
     // instrumentation (PICO_F_STATS)
     unsigned long long st_frontier;
     unsigned long long st_init_slots;
@@ -119,6 +127,7 @@ struct Ctrl {
     unsigned long long st_pushes;
     unsigned long long st_alive;
     unsigned long long st_fallback;
+    unsigned long long st_segs;
 };
 
 // Tunables (degree-class thresholds, bin caps).  PICO_F_TINY_TILES shrinks

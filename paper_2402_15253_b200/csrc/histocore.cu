@@ -328,18 +328,27 @@ __global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
 // lane locating its segment by a 5-step shuffle binary search.
 // ---------------------------------------------------------------------------
 template <bool STATS>
-__device__ void update_phase(const HcArgs &a, int t, long long gwarp, long long nwarps) {
+__device__ void update_phase(const HcArgs &a, int t) {
+    constexpr int U = 4;  // arcs in flight per lane (memory-level parallelism)
     const int lane = lane_id();
     const long long ns = (long long)ld_volatile(&a.ctl->nS[t & 1]);
+    const long long nbatch = (ns + 31) >> 5;
+    unsigned long long *wc = &a.ctl->wc[t & 1];
     unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
+    const unsigned lt_mask = (1u << lane) - 1;
     long long st_arcs = 0, st_guard = 0, st_push = 0;
-    for (long long base = gwarp * 32; base < ns; base += nwarps * 32) {
-        long long i = base + lane;
+    for (;;) {
+        // dynamic load balancing: a warp claims the next batch of 32 segments
+        long long bidx = 0;
+        if (lane == 0) bidx = (long long)atomicAdd(wc, 1ull);
+        bidx = __shfl_sync(FULL, bidx, 0);
+        if (bidx >= nbatch) break;
+        long long i = bidx * 32 + lane;
         long long b = 0;
         int len = 0, cv = 0, ov = 0;
         if (i < ns) {
             int2 sg = __ldcg(a.S + i);
-            long long r0 = a.rp[sg.x], r1 = a.rp[sg.x + 1];
+            long long r0 = __ldg(a.rp + sg.x), r1 = __ldg(a.rp + sg.x + 1);
             b = r0 + (long long)sg.y * a.tn.seg;
             len = (int)min((long long)a.tn.seg, r1 - b);
             cv = __ldcg(a.core + sg.x);
@@ -348,40 +357,73 @@ __device__ void update_phase(const HcArgs &a, int t, long long gwarp, long long 
         int incl = warp_incl_scan(len);
         int excl = incl - len;
         int total = __shfl_sync(FULL, incl, 31);
-        for (int j0 = 0; j0 < total; j0 += 32) {
-            int j = j0 + lane;
-            // owner = max lane with excl <= j
-            int lo = 0;
+        for (int j0 = 0; j0 < total; j0 += 32 * U) {
+            int u[U], cvo[U], ovo[U], cu[U];
+            bool ok[U], push[U];
+            long long hb[U];
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                int cand = lo + step;
-                int ex = __shfl_sync(FULL, excl, cand & 31);
-                if (cand < 32 && ex <= j) lo = cand;
+            for (int q = 0; q < U; q++) {
+                int j = j0 + q * 32 + lane;
+                int lo = 0;  // owner = max lane with excl <= j
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    int cand = lo + step;
+                    int ex = __shfl_sync(FULL, excl, cand & 31);
+                    if (cand < 32 && ex <= j) lo = cand;
+                }
+                long long eb = __shfl_sync(FULL, b, lo);
+                int ex = __shfl_sync(FULL, excl, lo);
+                cvo[q] = __shfl_sync(FULL, cv, lo);
+                ovo[q] = __shfl_sync(FULL, ov, lo);
+                ok[q] = j < total;
+                u[q] = ok[q] ? __ldg(a.ci + eb + (j - ex)) : 0;
             }
-            long long eb = __shfl_sync(FULL, b, lo);
-            int ex = __shfl_sync(FULL, excl, lo);
-            int cvo = __shfl_sync(FULL, cv, lo);
-            int ovo = __shfl_sync(FULL, ov, lo);
-            bool push = false;
-            int u = 0;
-            if (j < total) {
-                u = __ldg(a.ci + eb + (j - ex));
-                int cu = __ldcg(a.core + u);
-                if (STATS) st_arcs++;
-                if (cu > cvo) {  // N1/N3 neighbour
-                    long long hbu = a.rp[u] - 1;
-                    if (ovo >= cu) {
-                        int old = atomicSub(a.histo + hbu + cu, 1);  // cap bin
-                        push = (old == cu);
+#pragma unroll
+            for (int q = 0; q < U; q++) cu[q] = ok[q] ? __ldcg(a.core + u[q]) : 0;
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
+                hb[q] = ok[q] ? __ldg(a.rp + u[q]) - 1 : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                push[q] = false;
+                if (ok[q]) {
+                    if (ovo[q] >= cu[q]) {
+                        int old = atomicSub(a.histo + hb[q] + cu[q], 1);  // cap bin: cnt
+                        push[q] = (old == cu[q]);                          // exactly once
                     } else {
-                        atomicSub(a.histo + hbu + ovo, 1);
+                        red_add(a.histo + hb[q] + ovo[q], -1);
                     }
-                    atomicAdd(a.histo + hbu + cvo, 1);
-                    if (STATS) st_guard++;
+                    red_add(a.histo + hb[q] + cvo[q], 1);
                 }
             }
-            warp_append(push, u, a.F, nF);
-            if (STATS) st_push += push;
+            // one aggregated append of all pushes of the U sub-iterations
+            unsigned pm[U];
+            int tot = 0;
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                pm[q] = __ballot_sync(FULL, push[q]);
+                tot += __popc(pm[q]);
+            }
+            if (tot) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(nF, (unsigned long long)tot);
+                base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    if (push[q]) a.F[base + __popc(pm[q] & lt_mask)] = u[q];
+                    base += __popc(pm[q]);
+                }
+            }
+            if (STATS) {
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    st_arcs += (j0 + q * 32 + lane) < total;
+                    st_guard += ok[q];
+                    st_push += push[q];
+                }
+            }
         }
     }
     if (STATS) {
@@ -472,8 +514,12 @@ __global__ void __launch_bounds__(512) hc_rounds_kernel(HcArgs a) {
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     if (ld_volatile(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
     for (int t = 1;; t++) {
-        if (leader) a.ctl->nS[(t + 1) & 1] = 0;
-        update_phase<STATS>(a, t, gwarp, nwarps);
+        if (leader) {
+            a.ctl->nS[(t + 1) & 1] = 0;
+            a.ctl->wc[(t + 1) & 1] = 0;
+            if (STATS) a.ctl->st_segs += ld_volatile(&a.ctl->nS[t & 1]);
+        }
+        update_phase<STATS>(a, t);
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
         unsigned long long nf = ld_volatile(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
@@ -493,8 +539,12 @@ template <bool STATS>
 __global__ void __launch_bounds__(512) hc_update_kernel(HcArgs a, int t) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->nS[(t + 1) & 1] = 0;
-    update_phase<STATS>(a, t, gthread >> 5, nthreads >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->nS[(t + 1) & 1] = 0;
+        a.ctl->wc[(t + 1) & 1] = 0;
+        if (STATS) a.ctl->st_segs += a.ctl->nS[t & 1];
+    }
+    update_phase<STATS>(a, t);
 }
 
 template <bool STATS>
@@ -613,8 +663,10 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     tm.stop();
     if ((err = cudaGetLastError())) return err;
 
-    unsigned long long c1 = 0;
+    long long launches = 5;  // degree + 4 init kernels
+    unsigned long long c1 = 0, s1 = 0;
     if ((err = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return err;
+    if ((err = cudaMemcpyAsync(&s1, &a.ctl->nS[1], sizeof(s1), cudaMemcpyDeviceToHost, s))) return err;
     if ((err = cudaStreamSynchronize(s))) return err;
     // F_1 = C_1 (Theorem 2), recorded at fsz[0]
     unsigned long long rounds = c1 ? 1 : 0;
@@ -630,6 +682,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 tm.start(PICO_K_UPDATE);
                 hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t);
                 tm.stop();
+                launches++;
                 unsigned long long nf = 0;
                 if ((err = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf),
                                            cudaMemcpyDeviceToHost, s)))
@@ -642,6 +695,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 tm.start(PICO_K_SUM);
                 hc_sum_kernel<STATS><<<std::max(sb, 1), 512, 0, s>>>(a, t + 1);
                 tm.stop();
+                launches++;
             }
             if (STATS) {
                 unsigned long long tot = 0;
@@ -652,12 +706,13 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         } else {
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hc_rounds_kernel<STATS>, 512, 0);
-            int per = std::max(1, std::min(occ, 2));
+            int per = std::max(1, occ);
             int blocks = sms * per;
             void *args[] = {&a};
             tm.start(PICO_K_ROUNDS);
             err = cudaLaunchCooperativeKernel((const void *)hc_rounds_kernel<STATS>, blocks, 512, args, 0, s);
             tm.stop();
+            launches++;
             if (err) return err;
             unsigned long long devrounds = 0;
             if ((err = cudaMemcpyAsync(&devrounds, &a.ctl->rounds, sizeof(devrounds),
@@ -676,6 +731,8 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     if ((err = cudaGetLastError())) return err;
     if (st) {
         st->rounds = (int64_t)rounds;
+        st->kernel_count = launches;
+        st->segments_init = (int64_t)s1;
         if (st->frontier_sizes)
             for (size_t i = 0; i < hsz.size() && (int64_t)i < st->frontier_sizes_cap; i++)
                 st->frontier_sizes[i] = (int64_t)hsz[i];
@@ -692,6 +749,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
             st->bins_read = (int64_t)h.st_bins;
             st->pushes = (int64_t)h.st_pushes;
             st->hub_fallbacks = (int64_t)h.st_fallback;
+            st->segments = (int64_t)(h.st_segs + (c1 ? 0 : 0));
         }
     }
     tm.collect(st);

@@ -102,21 +102,28 @@ __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, 
     }
 }
 
-// drain of level k: process queue entries until none is pending
+// drain of level k: process queue entries until none is pending.  One thread
+// per CTA polls and claims a chunk of entries (CAS on the head); the CTA's
+// warps split the chunk 32 entries each and walk the rows with warp-level
+// load balancing; newly clamped vertices are pushed back into the queue.
 template <bool CLAMP_SUB, bool STATS>
 __device__ void po_drain_phase(const PoArgs &a, int k, int p) {
-    const int lane = lane_id();
+    __shared__ unsigned long long s_base;
+    __shared__ int s_got;
+    const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int kmin = INT_MAX;
     long long nproc = 0, st_arcs = 0, st_dec = 0;
     for (;;) {
-        unsigned long long base = 0;
-        int got = 0;
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
+            unsigned long long base = 0;
+            int got = 0;
             for (int spin = 0;; spin++) {
                 unsigned long long h = ld_volatile(&a.ctl->q_head);
                 unsigned long long t = ld_volatile(&a.ctl->q_tail);
                 if (h < t) {
-                    unsigned long long want = min(32ull, t - h);
+                    unsigned long long avail = t - h;
+                    unsigned long long share = (avail + gridDim.x - 1) / gridDim.x;
+                    unsigned long long want = min(avail, max(32ull, min((unsigned long long)(32 * nw), share)));
                     if (atomicCAS(&a.ctl->q_head, h, h + want) == h) {
                         base = h;
                         got = (int)want;
@@ -124,68 +131,75 @@ __device__ void po_drain_phase(const PoArgs &a, int k, int p) {
                     }
                 } else {
                     if (ld_volatile(&a.ctl->q_pending) == 0) break;
-                    __nanosleep(spin < 8 ? 32 : 256);
+                    __nanosleep(min(1024, 32 << min(spin, 5)));
                 }
             }
+            s_base = base;
+            s_got = got;
         }
-        got = __shfl_sync(FULL, got, 0);
+        __syncthreads();
+        const int got = s_got;
+        const unsigned long long base = s_base;
+        __syncthreads();
         if (got == 0) break;
-        base = __shfl_sync(FULL, base, 0);
-        long long b = 0;
-        int len = 0;
-        if (lane < got) {
-            long long e;
-            do {
-                e = *reinterpret_cast<volatile long long *>(a.Q + base + lane);
-            } while (e < 0);
-            int v = (int)(e >> 32);
-            int s = (int)(e & 0xffffffffll);
-            long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-            b = r0 + (long long)s * a.seg;
-            len = (int)min((long long)a.seg, r1 - b);
-        }
-        int incl = warp_incl_scan(len);
-        int excl = incl - len;
-        int total = __shfl_sync(FULL, incl, 31);
-        for (int j0 = 0; j0 < total; j0 += 32) {
-            int j = j0 + lane;
-            int lo = 0;
+        const int myn = min(32, got - wid * 32);
+        if (myn > 0) {
+            long long b = 0;
+            int len = 0;
+            if (lane < myn) {
+                long long e;
+                do {
+                    e = *reinterpret_cast<volatile long long *>(a.Q + base + wid * 32 + lane);
+                } while (e < 0);
+                int v = (int)(e >> 32);
+                int s = (int)(e & 0xffffffffll);
+                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+                b = r0 + (long long)s * a.seg;
+                len = (int)min((long long)a.seg, r1 - b);
+            }
+            int incl = warp_incl_scan(len);
+            int excl = incl - len;
+            int total = __shfl_sync(FULL, incl, 31);
+            for (int j0 = 0; j0 < total; j0 += 32) {
+                int j = j0 + lane;
+                int lo = 0;
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                int cand = lo + step;
-                int ex = __shfl_sync(FULL, excl, cand & 31);
-                if (cand < 32 && ex <= j) lo = cand;
-            }
-            long long eb = __shfl_sync(FULL, b, lo);
-            int ex = __shfl_sync(FULL, excl, lo);
-            bool push = false;
-            int u = 0;
-            if (j < total) {
-                u = __ldg(a.ci + eb + (j - ex));
-                int c = __ldcg(a.core + u);
-                if (STATS) st_arcs++;
-                if (c > k) {  // guard core[u] > k
-                    int old;
-                    if (CLAMP_SUB) {
-                        old = atomicSub(a.core + u, 1);
-                    } else {
-                        old = c;
-                        for (;;) {  // atomicSub>=k as a CAS loop
-                            if (old <= k) break;
-                            int prev = atomicCAS(a.core + u, old, old - 1);
-                            if (prev == old) break;
-                            old = prev;
-                        }
-                    }
-                    if (STATS) st_dec++;
-                    push = (old == k + 1);
-                    if (old - 1 > k) kmin = min(kmin, old - 1);
+                for (int step = 16; step >= 1; step >>= 1) {
+                    int cand = lo + step;
+                    int ex = __shfl_sync(FULL, excl, cand & 31);
+                    if (cand < 32 && ex <= j) lo = cand;
                 }
+                long long eb = __shfl_sync(FULL, b, lo);
+                int ex = __shfl_sync(FULL, excl, lo);
+                bool push = false;
+                int u = 0;
+                if (j < total) {
+                    u = __ldg(a.ci + eb + (j - ex));
+                    int c = __ldcg(a.core + u);
+                    if (STATS) st_arcs++;
+                    if (c > k) {  // guard core[u] > k
+                        int old;
+                        if (CLAMP_SUB) {
+                            old = atomicSub(a.core + u, 1);
+                        } else {
+                            old = c;
+                            for (;;) {  // atomicSub>=k as a CAS loop
+                                if (old <= k) break;
+                                int prev = atomicCAS(a.core + u, old, old - 1);
+                                if (prev == old) break;
+                                old = prev;
+                            }
+                        }
+                        if (STATS) st_dec++;
+                        push = (old == k + 1);
+                        if (old - 1 > k) kmin = min(kmin, old - 1);
+                    }
+                }
+                nproc += po_push(a, push, u);
             }
-            nproc += po_push(a, push, u);
         }
-        __syncwarp();
-        if (lane == 0) atomicAdd(&a.ctl->q_pending, 0ull - (unsigned long long)got);
+        __syncthreads();  // all pushes of this chunk precede its release
+        if (threadIdx.x == 0) atomicAdd(&a.ctl->q_pending, 0ull - (unsigned long long)got);
     }
     kmin = warp_min(kmin);
     if (lane == 0) {
@@ -363,6 +377,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     tstop();
     if ((err = cudaGetLastError())) return err;
 
+    long long launches = 1;
     tstart(PICO_K_PEEL);
     if (flags & PICO_F_HOST_LOOP) {
         int blocks = sms * 4;
@@ -373,17 +388,18 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
             Ctrl hc;
             if ((err = cudaMemcpyAsync(&hc, a.ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s))) return err;
             if ((err = cudaStreamSynchronize(s))) return err;
-            if (L > 0) po_close_kernel<<<1, 1, 0, s>>>(a, par ^ 1, kprev);
+            if (L > 0) { po_close_kernel<<<1, 1, 0, s>>>(a, par ^ 1, kprev); launches++; }
             if (hc.nAlive[par] == 0) break;
             k = std::max(k + 1, hc.kminb[par]);
             po_scan_kernel<STATS><<<blocks, 512, 0, s>>>(a, k, par);
             po_drain_kernel<CLAMP_SUB, STATS><<<blocks, 512, 0, s>>>(a, k, par);
+            launches += 2;
             if (CLAMP_SUB) {
                 unsigned long long lend = 0;
                 if ((err = cudaMemcpyAsync(&lend, &a.ctl->q_tail, sizeof(lend), cudaMemcpyDeviceToHost, s)))
                     return err;
                 if ((err = cudaStreamSynchronize(s))) return err;
-                if (lend > lstart) po_repair_kernel<<<blocks, 512, 0, s>>>(a, k, lstart, lend);
+                if (lend > lstart) { po_repair_kernel<<<blocks, 512, 0, s>>>(a, k, lstart, lend); launches++; }
                 lstart = lend;
             }
             kprev = k;
@@ -396,6 +412,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<CLAMP_SUB, STATS>, sms * per, 512,
                                           args, 0, s);
         if (err) return err;
+        launches++;
     }
     tstop();
     if ((err = cudaGetLastError())) return err;
@@ -409,6 +426,8 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     if ((err = cudaStreamSynchronize(s))) return err;
     if (st) {
         st->levels = (int64_t)hc.levels;
+        st->segments = (int64_t)hc.q_tail;
+        st->kernel_count = launches;
         st->subrounds = (int64_t)hc.scans;
         st->kmax = hc.kmax;
         if (st->frontier_sizes)
