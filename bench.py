@@ -45,20 +45,35 @@ def log(*a):
 # roofline model: algorithmic bytes per kernel slot (DESIGN.md "Algorithmic
 # bytes"; SURVEY 8(d) 4-byte access model, each logical access counted once)
 # ---------------------------------------------------------------------------
-def hc_bytes(n: int, m: int, st: dict, f1: int) -> dict:
+def hc_bytes(n: int, m: int, st: dict, f1: int, relabelled: bool = False) -> dict:
     arcs = 2 * m
     segs, s1 = st["segments"], st["segments_init"]
     degree = 8 * (n + 1) + 8 * n
     init = 8 * (n + 1) + 8 * arcs + 4 * st["init_slots_written"] + 4 * n + 8 * s1
     rounds = (32 * segs + 8 * st["arcs_scanned"] + 24 * st["guarded_arcs"] + 4 * st["pushes"]
-              + 36 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * (segs - s1))
-    return {"degree": degree, "init": init, "rounds": rounds}
+              + 36 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * (segs - s1)
+              + 10 * n * st.get("pull_rounds", 0))  # pull: rowptr + core16 of every row
+    out = {"degree": degree, "init": init, "rounds": rounds}
+    if relabelled:
+        out["relabel"] = relabel_bytes(n, m)
+    return out
 
 
-def po_bytes(n: int, m: int, st: dict) -> dict:
+def relabel_bytes(n: int, m: int) -> int:
+    """Internal relabel: degree keys (rowptr 8(n+1), keys+ids 8n), radix sort of
+    n (key, id) pairs (4 passes x 16 B), perm/rowptr2 (12n), row copy (rowptr
+    16 per row, colidx read + perm gather + colidx2 write = 12 per arc) and the
+    final coreness gather (12n)."""
+    return 8 * (n + 1) + 8 * n + 64 * n + 12 * n + 16 * n + 12 * 2 * m + 12 * n
+
+
+def po_bytes(n: int, m: int, st: dict, relabelled: bool = False) -> dict:
     degree = 8 * (n + 1) + 8 * n
     peel = 12 * st["alive_scanned"] + 32 * st["segments"] + 8 * st["arcs_scanned"] + 8 * st["guarded_arcs"]
-    return {"degree": degree, "peel": peel}
+    out = {"degree": degree, "peel": peel}
+    if relabelled:
+        out["relabel"] = relabel_bytes(n, m)
+    return out
 
 
 def hbm_peak():
@@ -232,7 +247,9 @@ def bench_single(args):
         # untimed instrumented run: iteration counts + work counters for B_alg
         st = pico.Stats()
         fs = np.zeros(1 << 16, dtype=np.int64)
-        core = pico.coreness(rp, ci, algo=algo, flags=pico.F_STATS, stats=st, frontier_sizes=fs)
+        ra = np.zeros(1 << 16, dtype=np.int64)
+        core = pico.coreness(rp, ci, algo=algo, flags=pico.F_STATS | args.flags, stats=st,
+                             frontier_sizes=fs, round_arcs=ra)
         torch.cuda.synchronize()
         sd = st.to_dict()
         # timed steps (per-kernel CUDA events recorded by the library, PICO_F_TIMING)
@@ -240,7 +257,7 @@ def bench_single(args):
 
         def step():
             s2 = pico.Stats()
-            pico.coreness(rp, ci, algo=algo, flags=pico.F_TIMING, stats=s2, out=core)
+            pico.coreness(rp, ci, algo=algo, flags=pico.F_TIMING | args.flags, stats=s2, out=core)
             d = s2.to_dict()
             for k, v in d["kernel_ms"].items():
                 acc["ms"][k] = acc["ms"].get(k, 0.0) + v
@@ -260,10 +277,11 @@ def bench_single(args):
             torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
         kms = {k: v / args.steps for k, v in acc["ms"].items()}
+        rl = "relabel" in kms
         if algo == "histocore":
-            byts = hc_bytes(n, m, sd, int(fs[0]) if sd["rounds"] > 0 else 0)
+            byts = hc_bytes(n, m, sd, int(fs[0]) if sd["rounds"] > 0 else 0, rl)
         else:
-            byts = po_bytes(n, m, sd)
+            byts = po_bytes(n, m, sd, rl)
         dom = max(kms, key=kms.get)
         ach = byts[dom] / (kms[dom] * 1e-3) / 1e9
         total_b = sum(byts.values())
@@ -273,7 +291,9 @@ def bench_single(args):
             "kernel_ms_per_step": kms, "alg_bytes": byts,
             "stats": {k: sd[k] for k in ("frontier_total", "init_slots_written", "arcs_scanned",
                                          "guarded_arcs", "bins_read", "pushes", "alive_scanned",
-                                         "segments", "hub_fallbacks")},
+                                         "segments", "hub_fallbacks", "pull_rounds")},
+            "frontier_sizes": [int(x) for x in fs[:min(max(sd["rounds"], sd["levels"]), 64)]],
+            "round_arcs": [int(x) for x in ra[:min(sd["rounds"], 64)]] if algo == "histocore" else None,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": ncu_traffic(args.config, algo, dom),
                          "peak_source": peak_src,
@@ -347,6 +367,7 @@ def main():
     ap.add_argument("--impl", default="pico", choices=["pico", "reference"])
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-both", dest="both", action="store_false")
+    ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rule)")

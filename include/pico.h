@@ -81,11 +81,23 @@ enum {
     PICO_F_HOST_LOOP = 8u,    /* one kernel launch per phase, host-driven    */
     PICO_F_CLAMP_SUB = 16u,   /* PeelOne: atomicSub + end-of-level repair    */
                               /* instead of the CAS clamp  */
-    PICO_F_TINY_TILES = 32u   /* test-only: tiny degree-class thresholds and */
+    PICO_F_TINY_TILES = 32u,  /* test-only: tiny degree-class thresholds and */
                               /* shared-memory bin caps so every code path   */
                               /* (incl. the global-histogram fallback) runs  */
                               /* on small graphs                             */
+    PICO_F_PUSH_ONLY = 64u,   /* HistoCore: never use the pull-direction     */
+                              /* UpdateHisto (dense rounds)                  */
+    PICO_F_PULL_ALWAYS = 128u,/* HistoCore: pull direction in every round    */
+    PICO_F_RELABEL = 256u,    /* force the internal compaction of isolated   */
+                              /* vertex ids (result mapped back, bit-exact)  */
+    PICO_F_NO_RELABEL = 512u  /* never compact (default: compact when n >=   */
+                              /* pico_relabel_threshold() and >= 10% of the  */
+                              /* ids are isolated, so per-vertex arrays fit  */
+                              /* the L2)                                     */
 };
+
+/* Vertex count above which pico_coreness_ex relabels internally by default. */
+int64_t pico_relabel_threshold(void);
 
 /* kernel slots of pico_stats_t.kernel_ms / kernel_launches */
 enum {
@@ -121,6 +133,7 @@ typedef struct {
                                 /* produced; PeelOne: queue entries processed  */
     int64_t segments_init;      /* HistoCore: of which produced by init        */
     int64_t kernel_count;       /* kernels this library launched in the call   */
+    int64_t pull_rounds;        /* HistoCore: rounds run in the pull direction */
     /* per-kernel device time (PICO_F_TIMING) */
     double kernel_ms[PICO_K_COUNT];
     int64_t kernel_launches[PICO_K_COUNT];
@@ -128,6 +141,9 @@ typedef struct {
      * (HistoCore) or the processed count per level (PeelOne); may be NULL */
     int64_t *frontier_sizes;
     int64_t frontier_sizes_cap;
+    /* optional caller-owned HOST array (same capacity) receiving, for
+     * HistoCore, sum_{v in C_t} deg(v) for t = 1..rounds; may be NULL */
+    int64_t *round_arcs;
 } pico_stats_t;
 
 /* The north-star entry point: coreness of every vertex, device buffers. */

@@ -15,11 +15,12 @@ import ctypes
 
 import numpy as np
 
-from ._lib import (ALGOS, F_CLAMP_SUB, F_HOST_LOOP, F_STATS, F_TIMING, F_TINY_TILES,  # noqa: F401
-                   F_VALIDATE, PicoError, Stats, check, header_functions, load)
+from ._lib import (ALGOS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
+                   F_RELABEL, F_STATS, F_TIMING, F_TINY_TILES, F_VALIDATE, PicoError, Stats, check, header_functions, load)
 
 __all__ = ["coreness", "coreness_host", "workspace_bytes", "PicoError", "Stats", "load",
-           "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES"]
+           "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES",
+           "F_PUSH_ONLY", "F_PULL_ALWAYS", "F_RELABEL", "F_NO_RELABEL"]
 
 
 def _algo(algo) -> int:
@@ -35,7 +36,7 @@ def workspace_bytes(n: int, m: int, algo="histocore", flags: int = 0) -> int:
 
 
 def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspace=None,
-             stats: Stats | None = None, frontier_sizes=None, stream=None):
+             stats: Stats | None = None, frontier_sizes=None, round_arcs=None, stream=None):
     """Coreness of every vertex of a symmetric deduplicated CSR graph held in
     device memory (``pico_coreness_ex``).
 
@@ -70,6 +71,9 @@ def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspa
             st = Stats()
         st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         st.frontier_sizes_cap = frontier_sizes.size
+        if round_arcs is not None:
+            assert round_arcs.size >= frontier_sizes.size
+            st.round_arcs = round_arcs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
     with torch.cuda.device(rowptr.device):
         rc = lib.pico_coreness_ex(rowptr.data_ptr(), colidx.data_ptr() if arcs else None, n, m, _algo(algo),
                                   out.data_ptr() if n > 0 else None, ctypes.c_void_p(stream.cuda_stream), flags,

@@ -18,8 +18,12 @@ F_TIMING = 4
 F_HOST_LOOP = 8
 F_CLAMP_SUB = 16
 F_TINY_TILES = 32
+F_PUSH_ONLY = 64
+F_PULL_ALWAYS = 128
+F_RELABEL = 256
+F_NO_RELABEL = 512
 
-K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "other"]
+K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel"]
 
 STATUS = {0: "PICO_OK", 1: "PICO_EINVAL", 2: "PICO_ENOTSUP", 3: "PICO_ENOMEM",
           4: "PICO_ECUDA", 5: "PICO_ENCCL", 6: "PICO_EGRAPH"}
@@ -50,14 +54,16 @@ class Stats(ctypes.Structure):
         ("segments", ctypes.c_int64),
         ("segments_init", ctypes.c_int64),
         ("kernel_count", ctypes.c_int64),
+        ("pull_rounds", ctypes.c_int64),
         ("kernel_ms", ctypes.c_double * 8),
         ("kernel_launches", ctypes.c_int64 * 8),
         ("frontier_sizes", ctypes.POINTER(ctypes.c_int64)),
         ("frontier_sizes_cap", ctypes.c_int64),
+        ("round_arcs", ctypes.POINTER(ctypes.c_int64)),
     ]
 
     def to_dict(self) -> dict:
-        d = {k: int(getattr(self, k)) for k, _ in self._fields_[:15]}
+        d = {k: int(getattr(self, k)) for k, _ in self._fields_[:16]}
         d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(8) if self.kernel_launches[i]}
         d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(8) if self.kernel_launches[i]}
         return d
@@ -85,7 +91,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB
+    p = path or os.environ.get("PICO_LIB") or LIB
     if not os.path.exists(p):
         raise OSError(f"libpico.so not built ({p}); run `python -m paper_2402_15253_b200.build` "
                       "or __graft_entry__.build()")
@@ -105,6 +111,8 @@ def load(path: str | None = None):
     lib.pico_last_error.restype = ctypes.c_char_p
     lib.pico_version.argtypes = []
     lib.pico_version.restype = i32
+    lib.pico_relabel_threshold.argtypes = []
+    lib.pico_relabel_threshold.restype = i64
     _setup_shard(lib)
     _lib = lib
     return lib

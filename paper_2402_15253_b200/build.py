@@ -45,16 +45,18 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    target = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I" + INCLUDE, "-I" + CSRC, "-o", tmp] + sources()
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = ([nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines]
+           + ["-I" + INCLUDE, "-I" + CSRC, "-o", tmp] + sources())
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -126,11 +126,12 @@ static cudaError_t dev_info(DevInfo *d) {
 
 static void reset_stats(pico_stats_t *st) {
     if (!st) return;
-    int64_t *fs = st->frontier_sizes;
+    int64_t *fs = st->frontier_sizes, *ra = st->round_arcs;
     int64_t cap = st->frontier_sizes_cap;
     memset(st, 0, sizeof(*st));
     st->frontier_sizes = fs;
     st->frontier_sizes_cap = cap;
+    st->round_arcs = ra;
 }
 
 extern "C" {
@@ -152,12 +153,26 @@ const char *pico_last_error(void) { return g_last_error.c_str(); }
 
 int pico_version(void) { return 100; }
 
+static const long long kRelabelMinN = 16ll << 20;  // per-vertex arrays beyond L2 reach
+
+int64_t pico_relabel_threshold(void) { return kRelabelMinN; }
+
+static bool use_relabel(long long n, long long m, uint32_t flags) {
+    if (m <= 0 || (flags & PICO_F_NO_RELABEL)) return false;
+    return (flags & PICO_F_RELABEL) || n >= kRelabelMinN;
+}
+
+static size_t algo_bytes(long long n, long long arcs, int algo, uint32_t flags) {
+    if (algo == PICO_ALGO_HISTOCORE) return hc_workspace_bytes(n, arcs, flags);
+    if (algo == PICO_ALGO_PEELONE) return po_workspace_bytes(n, arcs, flags);
+    return 0;
+}
+
 size_t pico_workspace_bytes(int64_t n, int64_t m, int algo, uint32_t flags) {
     if (n <= 0 || m < 0) return 256;
     long long arcs = 2 * (long long)m;
-    size_t b = 0;
-    if (algo == PICO_ALGO_HISTOCORE) b = hc_workspace_bytes(n, arcs, flags);
-    else if (algo == PICO_ALGO_PEELONE) b = po_workspace_bytes(n, arcs, flags);
+    size_t b = algo_bytes(n, arcs, algo, flags);
+    if (use_relabel(n, m, flags)) b = ((b + 255) & ~size_t(255)) + relabel_workspace_bytes(n, arcs);
     return std::max<size_t>(b, 256);
 }
 
@@ -208,11 +223,65 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
             if (e) rc = cuda_fail(e, "zero core_out");
         } else {
             if (!dev.coop && !(flags & PICO_F_HOST_LOOP)) flags |= PICO_F_HOST_LOOP;
-            if (algo == PICO_ALGO_HISTOCORE)
-                e = hc_run(rp, colidx, n, arcs, core_out, s, flags, ws, stats, dev);
-            else
-                e = po_run(rp, colidx, n, arcs, core_out, s, flags, ws, stats, dev);
-            if (e) rc = cuda_fail(e, algo == PICO_ALGO_HISTOCORE ? "histocore" : "peelone");
+            const long long *grp = rp;
+            const int *gci = colidx;
+            long long gn = n;
+            int *gcore = core_out;
+            Relabel rl{};
+            bool relabel = use_relabel(n, m, flags);
+            void *aws = ws;
+            cudaEvent_t r0 = nullptr, r1 = nullptr;
+            bool timing = stats && (flags & PICO_F_TIMING);
+            if (relabel) {
+                size_t ab = (algo_bytes(n, arcs, algo, flags) + 255) & ~size_t(255);
+                if (timing) {
+                    cudaEventCreate(&r0);
+                    cudaEventCreate(&r1);
+                    cudaEventRecord(r0, s);
+                }
+                e = relabel_build(rp, colidx, n, arcs, s, (char *)ws + ab, dev, (flags & PICO_F_RELABEL) != 0, &rl);
+                if (e) rc = cuda_fail(e, "relabel");
+                if (timing) cudaEventRecord(r1, s);
+                if (rl.active) {
+                    grp = rl.rp2;
+                    gci = rl.ci2;
+                    gn = rl.n2;
+                    gcore = rl.core2;
+                } else {
+                    if (stats) stats->kernel_count += rl.launches;
+                    relabel = false;
+                }
+            }
+            if (rc == PICO_OK) {
+                if (algo == PICO_ALGO_HISTOCORE)
+                    e = hc_run(grp, gci, gn, arcs, gcore, s, flags, aws, stats, dev);
+                else
+                    e = po_run(grp, gci, gn, arcs, gcore, s, flags, aws, stats, dev);
+                if (e) rc = cuda_fail(e, algo == PICO_ALGO_HISTOCORE ? "histocore" : "peelone");
+            }
+            if (rc == PICO_OK && relabel) {
+                cudaEvent_t b0 = nullptr, b1 = nullptr;
+                if (timing) {
+                    cudaEventCreate(&b0);
+                    cudaEventCreate(&b1);
+                    cudaEventRecord(b0, s);
+                }
+                e = relabel_back(rl, n, core_out, s, dev);
+                if (timing) cudaEventRecord(b1, s);
+                if (!e) e = cudaStreamSynchronize(s);
+                if (e) rc = cuda_fail(e, "relabel back");
+                if (stats) stats->kernel_count += rl.launches + 1;
+                if (timing && rc == PICO_OK) {
+                    float t1 = 0, t2 = 0;
+                    cudaEventElapsedTime(&t1, r0, r1);
+                    cudaEventElapsedTime(&t2, b0, b1);
+                    stats->kernel_ms[PICO_K_OTHER] += t1 + t2;
+                    stats->kernel_launches[PICO_K_OTHER] += 1;
+                }
+                if (b0) { cudaEventDestroy(b0); cudaEventDestroy(b1); }
+            }
+            if (r0) { cudaEventDestroy(r0); cudaEventDestroy(r1); }
+            e = cudaSuccess;
             if (!e && stats && algo == PICO_ALGO_HISTOCORE) {
                 int *d = (int *)ws;  // Ctrl region is free again
                 int km = 0;

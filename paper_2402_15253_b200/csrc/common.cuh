@@ -66,6 +66,63 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
     return *reinterpret_cast<const volatile unsigned long long *>(p);
 }
 
+// L2 eviction-priority policies (createpolicy) and loads carrying them:
+// streaming data (colidx, work lists) is evict_first so it does not flush the
+// hot random-access structures (8-bit estimate shadow, changed bitmap), which
+// are evict_last.
+__device__ __forceinline__ unsigned long long pol_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long pol_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only streaming load (never written during the kernel)
+__device__ __forceinline__ int ld_stream(const int *p, unsigned long long pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ long long ld_stream64(const long long *p, unsigned long long pol) {
+    long long v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// coherent (L2) loads of data other CTAs may have written before a barrier
+__device__ __forceinline__ unsigned ld_cg_u8(const unsigned char *p, unsigned long long pol) {
+    unsigned short v;
+    asm volatile("ld.global.cg.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_cg_u16(const unsigned short *p, unsigned long long pol) {
+    unsigned short v;
+    asm volatile("ld.global.cg.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_cg_u32(const unsigned *p, unsigned long long pol) {
+    unsigned v;
+    asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int2 ld_stream_int2(const int2 *p, unsigned long long pol) {
+    int2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+#ifndef PICO_L2_HINTS
+#define PICO_L2_HINTS 0
+#endif
+#if !PICO_L2_HINTS
+// hints disabled: plain cached loads
+#define ld_stream(p, pol) __ldg(p)
+#define ld_stream_int2(p, pol) __ldcg(p)
+#define ld_cg_u32(p, pol) __ldcg(p)
+#endif
+
 // fire-and-forget global reduction (REDG), relaxed, device scope
 __device__ __forceinline__ void red_add(int *p, int v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -102,6 +159,9 @@ struct Ctrl {
     unsigned long long nX;         // hub fallback list (global bins)
     unsigned long long rounds;     // HistoCore rounds >= 2 counted on device
     unsigned long long wc[2];      // UpdateHisto batch claim counters (parity)
+    unsigned long long arcsC[2];   // sum of deg(v) over C_t (parity t&1)
+    int mincv[2];                  // min core_t(v) over C_t (parity t&1)
+    unsigned long long nH;         // static hub segments (pull mode)
     // PeelOne queue state (a run-wide log of processed (vertex, segment)s);
     // each hot word on its own 128-byte line (polling vs. atomics)
     alignas(128) unsigned long long q_head;     // next queue slot to claim
@@ -128,6 +188,7 @@ struct Ctrl {
     unsigned long long st_alive;
     unsigned long long st_fallback;
     unsigned long long st_segs;
+    unsigned long long st_pull;
 };
 
 // Tunables (degree-class thresholds, bin caps).  PICO_F_TINY_TILES shrinks
@@ -137,6 +198,7 @@ struct Tune {
     int b_max;      // class B (warp per vertex):   a_max < deg <= b_max
     int c_bins;     // class C (CTA per vertex) shared-memory bin cap
     int seg;        // arcs per UpdateHisto segment
+    int pull_div;   // pull-mode UpdateHisto when arcs(C_t) >= 2m / pull_div
 };
 
 }  // namespace pico

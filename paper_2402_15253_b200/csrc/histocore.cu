@@ -2,6 +2,10 @@
 //
 // State in HBM:
 //   core[v]   int32   current estimate h_t(v) (= core_out; P:495 core <- deg)
+//   c8[v]     uint8   min(core[v], 255): an L2-resident shadow used by every
+//                     neighbour gather (exact below the saturation value; a
+//                     saturated entry falls back to core[v]; before the
+//                     rounds it holds min(deg(v), 255) for InitHisto)
 //   oldc[v]   int32   estimate before v's latest change (oldcore); during
 //                     init it holds deg(v), the round-0 estimate of every vertex
 //   histo     int32[2m], vertex v owns slots rowptr[v] + b - 1 for bins
@@ -13,46 +17,99 @@
 //   F         int32   frontier list F_t (Theorem 2: cnt < core)
 //   S         int2    UpdateHisto work list: (v, segment) for every changed v,
 //                     one entry per `seg` arcs of v's row (load balance)
+//   H         int2    static (v, segment) list of the hub rows (deg > seg) for
+//                     the pull-mode UpdateHisto
+//   chg[2]    bitmap  changed set C_t (parity t&1) for pull mode
 //
 // Round structure (strict two-phase synchronous rounds):
 //   init   = InitHisto fused with round-1 SumHisto: per vertex a
 //            capped histogram of min(deg(u), deg(v)) in registers / shared
-//            memory, its h-index, and only bins 1..h written back (the stale
-//            bins above the cap are never read).  Changed vertices -> S.
-//   loop   { UpdateHisto(S) -> F_{t+1} ; SumHisto(F_{t+1}) -> S }  until F empty
+//            memory, its h-index, and only bins 1..h written back.
+//   loop   { UpdateHisto(C_t) -> F_{t+1} ; SumHisto(F_{t+1}) -> C_{t+1} }
 // UpdateHisto: for v in C_t, u in nbr(v) with core[u] > core[v]:
 //   old = atomicSub(histo[u][min(oldcore[v], core[u])], 1);
 //   atomicAdd(histo[u][core[v]], 1);
 //   push u iff oldcore[v] >= core[u] and old == core[u]   (exactly once,
 //   the cap bin is only ever decremented).
+//   Two bit-exact directions apply the SAME (v, u) bin moves:
+//     push: changed rows are scanned, the moves hit u's histogram remotely;
+//     pull (dense rounds): every row u with core[u] > min core_t(C_t) is
+//       streamed, v is tested against the changed bitmap, the moves hit u's
+//       own histogram region (L2-local atomics).
 // SumHisto: walk k = core_old, core_old-1, ...; sum += histo[v][k];
 //   stop at the first k with sum >= k; core[v] = k,
 //   oldcore[v] = core_old, histo[v][k] = sum.
+#include <climits>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pico {
 
+// build-time A/B knobs: shadow width (8 or 16 bits) and L2 eviction hints
+#ifndef PICO_SHADOW_BITS
+#define PICO_SHADOW_BITS 16
+#endif
+#ifndef PICO_L2_HINTS
+#define PICO_L2_HINTS 0
+#endif
+#if PICO_SHADOW_BITS == 8
+typedef unsigned char shadow_t;
+constexpr unsigned SAT8 = 255;
+#else
+typedef unsigned short shadow_t;
+constexpr unsigned SAT8 = 65535;
+#endif
+
 struct HcArgs {
     const long long *rp;   // rowptr [n+1]
     const int *ci;         // colidx [2m]
     int n;
+    long long arcs;
     int *core;             // [n]  (core_out)
+    shadow_t *c8;          // [n]  saturated shadow of core
     int *oldc;             // [n]
     int *histo;            // [2m]
     int *F;                // [n]  frontier list; init: hub fallback list
     int *BC;               // [n]  init class lists (B from front, C from back)
-    int2 *S;               // [n + 2m/seg + 32] update segments
+    int2 *S;               // update segments of C_t
+    int2 *H;               // static hub segments (pull mode)
+    unsigned *chg;         // [2][nwords] changed bitmaps
+    long long nwords;
     unsigned long long *fsz;  // [fsz_cap] per-round frontier sizes
+    unsigned long long *rarcs;  // [fsz_cap] per-round arcs of C_t (stats)
     unsigned long long fsz_cap;
     Ctrl *ctl;
     Tune tn;
+    int allow_pull;
 };
 
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int nseg_of(long long d, int seg) { return (int)((d + seg - 1) / seg); }
+
+// exact estimate of u through the 8-bit shadow (hot policy)
+__device__ __forceinline__ unsigned ld_shadow(const shadow_t *p, unsigned long long hot) {
+#if PICO_L2_HINTS
+#if PICO_SHADOW_BITS == 8
+    return ld_cg_u8(p, hot);
+#else
+    return ld_cg_u16(p, hot);
+#endif
+#else
+    return __ldcg(p);
+#endif
+}
+
+__device__ __forceinline__ int core_of(const HcArgs &a, int u, unsigned long long hot) {
+    unsigned c = ld_shadow(a.c8 + u, hot);
+    return c == SAT8 ? __ldcg(a.core + u) : (int)c;
+}
+
+__device__ __forceinline__ void set_c8(const HcArgs &a, int v, int k) {
+    a.c8[v] = (shadow_t)min(k, (int)SAT8);
+}
 
 // warp-aggregated reservation of nseg segments per lane; writes (v, s) entries
 __device__ __forceinline__ void warp_append_segments(int v, int nseg, int2 *S,
@@ -72,8 +129,32 @@ __device__ __forceinline__ void stat_add(unsigned long long *ctr, long long x) {
     if (lane_id() == 0 && s) atomicAdd(ctr, (unsigned long long)s);
 }
 
+// Bookkeeping of the changed set C_t for round t's UpdateHisto: |C_t|, arcs
+// of C_t, minimum new estimate (accumulated per thread, flushed once per
+// phase -- these are single-address counters) and the changed bitmap.
+struct ChangeAcc {
+    long long cnt = 0, arcs = 0;
+    int kmin = INT_MAX;
+    __device__ __forceinline__ void note(const HcArgs &a, int t, int v, int k, long long d) {
+        cnt++;
+        arcs += d;
+        kmin = min(kmin, k);
+        atomicOr(a.chg + (t & 1) * a.nwords + (v >> 5), 1u << (v & 31));
+    }
+    // all 32 lanes call; count_into: counter of |C_t| (init only) or null
+    __device__ __forceinline__ void flush(const HcArgs &a, int t, unsigned long long *count_into) {
+        long long c = warp_sum64(cnt), s = warp_sum64(arcs);
+        int km = warp_min(kmin);
+        if (lane_id() == 0 && c) {
+            atomicAdd(&a.ctl->arcsC[t & 1], (unsigned long long)s);
+            atomicMin(&a.ctl->mincv[t & 1], km);
+            if (count_into) atomicAdd(count_into, (unsigned long long)c);
+        }
+    }
+};
+
 // ---------------------------------------------------------------------------
-// H0: degrees + classification
+// H0: degrees, classification, hub segment list, 16-bit shadow
 // ---------------------------------------------------------------------------
 __global__ void hc_degree_kernel(HcArgs a) {
     long long nthreads = (long long)gridDim.x * blockDim.x;
@@ -85,6 +166,7 @@ __global__ void hc_degree_kernel(HcArgs a) {
         if (valid) {
             a.oldc[v] = (int)d;  // round-0 estimate of every vertex
             a.core[v] = (int)d;
+            set_c8(a, v, (int)d);
         }
         bool isB = valid && d > a.tn.a_max && d <= a.tn.b_max;
         bool isC = valid && d > a.tn.b_max;
@@ -98,7 +180,16 @@ __global__ void hc_degree_kernel(HcArgs a) {
             base = __shfl_sync(FULL, base, leader);
             if (isC) a.BC[a.n - 1 - (long long)(base + __popc(m & ((1u << lane_id()) - 1)))] = v;
         }
+        warp_append_segments(v, (valid && d > a.tn.seg) ? nseg_of(d, a.tn.seg) : 0, a.H, &a.ctl->nH);
     }
+}
+
+// neighbour degree for init, clamped to d (the histogram cap of P:498)
+__device__ __forceinline__ int init_val(const HcArgs &a, int u, int d, unsigned long long hot) {
+    int x = (int)ld_shadow(a.c8 + u, hot);
+    if (x >= d) return d;
+    if (x == (int)SAT8) return min(__ldg(a.oldc + u), d);
+    return x;
 }
 
 // ---------------------------------------------------------------------------
@@ -110,6 +201,9 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
     constexpr int NB = 16;
     long long nthreads = (long long)gridDim.x * blockDim.x;
     long long iters = ((long long)a.n + nthreads - 1) / nthreads;
+    ChangeAcc acc;
+    long long st_slots = 0;
+    const unsigned long long hot = pol_last(), cold = pol_first();
     for (long long it = 0; it < iters; it++) {
         int v = (int)(it * nthreads + blockIdx.x * blockDim.x + threadIdx.x);
         bool valid = v < a.n;
@@ -126,8 +220,7 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
 #pragma unroll
             for (int b = 0; b < NB; b++) cnt[b] = 0;
             for (int e = 0; e < d; e++) {
-                int u = __ldg(a.ci + hb + e);
-                int x = min(__ldg(a.oldc + u), d);  // min(core[u], core[v])
+                int x = init_val(a, ld_stream(a.ci + hb + e, cold), d, hot);  // min(core[u], core[v])
 #pragma unroll
                 for (int b = 0; b < NB; b++) cnt[b] += (x == b + 1);
             }
@@ -147,12 +240,12 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
             a.core[v] = h;
             if (h < d) nseg = nseg_of(d, a.tn.seg);
         }
-        bool changed = nseg > 0;
-        unsigned cm = __ballot_sync(FULL, changed);
-        if (lane_id() == 0 && cm) atomicAdd(&a.ctl->nF[1], (unsigned long long)__popc(cm));
+        if (nseg > 0) acc.note(a, 1, v, h, d);
         warp_append_segments(v, nseg, a.S, &a.ctl->nS[1]);
-        if (STATS) stat_add(&a.ctl->st_init_slots, mine ? h : 0);
+        if (STATS && mine) st_slots += h;
     }
+    acc.flush(a, 1, &a.ctl->nF[1]);
+    if (STATS) stat_add(&a.ctl->st_init_slots, st_slots);
 }
 
 // ---------------------------------------------------------------------------
@@ -167,17 +260,16 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
     const long long nB = (long long)a.ctl->nB;
     const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    ChangeAcc acc;
+    long long st_slots = 0;
+    const unsigned long long hot = pol_last(), cold = pol_first();
     for (long long idx = gw; idx < nB; idx += nw) {
         int v = a.BC[idx];
         long long hb = a.rp[v];
         int d = (int)(a.rp[v + 1] - hb);
         for (int b = lane; b <= d; b += 32) bins[b] = 0;
         __syncwarp();
-        for (int e = lane; e < d; e += 32) {
-            int u = __ldg(a.ci + hb + e);
-            int x = min(__ldg(a.oldc + u), d);
-            atomicAdd(&bins[x], 1);
-        }
+        for (int e = lane; e < d; e += 32) atomicAdd(&bins[init_val(a, ld_stream(a.ci + hb + e, cold), d, hot)], 1);
         __syncwarp();
         // descending walk for the h-index (SumHisto on the fresh histogram)
         int carry = 0, top = d, h = 0, hs = 0;
@@ -201,8 +293,8 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         int nseg = (h < d) ? nseg_of(d, a.tn.seg) : 0;
         if (lane == 0) {
             a.core[v] = h;
-            if (nseg) atomicAdd(&a.ctl->nF[1], 1ull);
-            if (STATS) atomicAdd(&a.ctl->st_init_slots, (unsigned long long)h);
+            if (nseg) acc.note(a, 1, v, h, d);
+            st_slots += h;
         }
         if (nseg) {
             unsigned long long base = 0;
@@ -211,6 +303,8 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
             for (int s = lane; s < nseg; s += 32) a.S[base + s] = make_int2(v, s);
         }
     }
+    acc.flush(a, 1, &a.ctl->nF[1]);
+    if (STATS) stat_add(&a.ctl->st_init_slots, st_slots);
 }
 
 // ---------------------------------------------------------------------------
@@ -229,19 +323,16 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
     for (int b = tid; b <= B; b += nt)
         if (!GLOBAL || b >= 1) bins[b] = 0;
     __syncthreads();
-    for (int e = tid; e < d; e += nt) {
-        int u = __ldg(a.ci + hb + e);
-        int x = min(__ldg(a.oldc + u), B);
-        atomicAdd(&bins[x], 1);
-    }
+    const unsigned long long hot = pol_last(), cold = pol_first();
+    for (int e = tid; e < d; e += nt)
+        atomicAdd(&bins[min(init_val(a, ld_stream(a.ci + hb + e, cold), d, hot), B)], 1);
     __syncthreads();
     // block-wide descending search: h = max b in 1..B with sum_{j>=b} bins[j] >= b
     int c = (B + nt - 1) / nt;
-    int hiT = B - tid * c;              // this thread's chunk, descending
+    int hiT = B - tid * c;  // this thread's chunk, descending
     int loT = max(1, B - (tid + 1) * c + 1);
     int tsum = 0;
     for (int b = hiT; b >= loT; b--) tsum += bins[b];
-    // block exclusive scan of tsum in thread order
     int incl = warp_incl_scan(tsum);
     if (lane == 31) red[wid] = incl;
     __syncthreads();
@@ -285,6 +376,9 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
         a.core[v] = h;
         if (nseg) {
             atomicAdd(&a.ctl->nF[1], 1ull);
+            atomicAdd(&a.ctl->arcsC[1], (unsigned long long)d);
+            atomicMin(&a.ctl->mincv[1], h);
+            atomicOr(a.chg + a.nwords + (v >> 5), 1u << (v & 31));
             red[34] = (int)atomicAdd(&a.ctl->nS[1], (unsigned long long)nseg);
         }
         if (STATS) {
@@ -321,24 +415,70 @@ __global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
     }
 }
 
+// after init: the shadow switches from degrees to the round-1 estimates
+__global__ void hc_shadow_kernel(HcArgs a) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += nthreads)
+        set_c8(a, (int)v, a.core[v]);
+}
+
 // ---------------------------------------------------------------------------
-// UpdateHisto phase of round t: segments of C_t (count nS[t&1]) -> F_{t+1}
-// (count nF[(t+1)&1]).  Warp-centric load balancing: a warp takes 32 segments,
-// scans their lengths, and walks the concatenated arcs 32 at a time, each
-// lane locating its segment by a 5-step shuffle binary search.
+// one (v, u) bin move of UpdateHisto on u's histogram (hbu = rowptr[u] - 1):
+// returns true iff this call drove cnt(u) below core[u] (the push)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool bin_move(int *histo, long long hbu, int cu, int cv, int ov) {
+    bool push = false;
+    if (ov >= cu) {
+        int old = atomicSub(histo + hbu + cu, 1);  // cap bin: cnt
+        push = (old == cu);                        // exactly once
+    } else {
+        red_add(histo + hbu + ov, -1);
+    }
+    red_add(histo + hbu + cv, 1);
+    return push;
+}
+
+// warp-aggregated append of up to U pushes per lane to F
+template <int U>
+__device__ __forceinline__ void append_pushes(const bool (&push)[U], const int (&u)[U], int *F,
+                                              unsigned long long *nF) {
+    const unsigned lt_mask = (1u << lane_id()) - 1;
+    unsigned pm[U];
+    int tot = 0;
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        pm[q] = __ballot_sync(FULL, push[q]);
+        tot += __popc(pm[q]);
+    }
+    if (tot) {
+        unsigned long long base = 0;
+        if (lane_id() == 0) base = atomicAdd(nF, (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            if (push[q]) F[base + __popc(pm[q] & lt_mask)] = u[q];
+            base += __popc(pm[q]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// UpdateHisto, push direction, round t: segments of C_t (count nS[t&1]) ->
+// F_{t+1} (count nF[(t+1)&1]).  Warps claim batches of 32 segments, scan
+// their lengths, and walk the concatenated arcs U*32 at a time (owner lane by
+// a 5-step shuffle binary search), U arcs in flight per lane.
 // ---------------------------------------------------------------------------
 template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
-    constexpr int U = 4;  // arcs in flight per lane (memory-level parallelism)
+    constexpr int U = 4;
     const int lane = lane_id();
     const long long ns = (long long)ld_volatile(&a.ctl->nS[t & 1]);
     const long long nbatch = (ns + 31) >> 5;
     unsigned long long *wc = &a.ctl->wc[t & 1];
     unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
-    const unsigned lt_mask = (1u << lane) - 1;
     long long st_arcs = 0, st_guard = 0, st_push = 0;
+    const unsigned long long hot = pol_last(), cold = pol_first();
     for (;;) {
-        // dynamic load balancing: a warp claims the next batch of 32 segments
         long long bidx = 0;
         if (lane == 0) bidx = (long long)atomicAdd(wc, 1ull);
         bidx = __shfl_sync(FULL, bidx, 0);
@@ -347,7 +487,7 @@ __device__ void update_phase(const HcArgs &a, int t) {
         long long b = 0;
         int len = 0, cv = 0, ov = 0;
         if (i < ns) {
-            int2 sg = __ldcg(a.S + i);
+            int2 sg = ld_stream_int2(a.S + i, cold);
             long long r0 = __ldg(a.rp + sg.x), r1 = __ldg(a.rp + sg.x + 1);
             b = r0 + (long long)sg.y * a.tn.seg;
             len = (int)min((long long)a.tn.seg, r1 - b);
@@ -360,7 +500,6 @@ __device__ void update_phase(const HcArgs &a, int t) {
         for (int j0 = 0; j0 < total; j0 += 32 * U) {
             int u[U], cvo[U], ovo[U], cu[U];
             bool ok[U], push[U];
-            long long hb[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 int j = j0 + q * 32 + lane;
@@ -376,50 +515,130 @@ __device__ void update_phase(const HcArgs &a, int t) {
                 cvo[q] = __shfl_sync(FULL, cv, lo);
                 ovo[q] = __shfl_sync(FULL, ov, lo);
                 ok[q] = j < total;
-                u[q] = ok[q] ? __ldg(a.ci + eb + (j - ex)) : 0;
+                u[q] = ok[q] ? ld_stream(a.ci + eb + (j - ex), cold) : 0;
             }
 #pragma unroll
-            for (int q = 0; q < U; q++) cu[q] = ok[q] ? __ldcg(a.core + u[q]) : 0;
+            for (int q = 0; q < U; q++) cu[q] = ok[q] ? core_of(a, u[q], hot) : 0;
 #pragma unroll
             for (int q = 0; q < U; q++) {
+                if (STATS) st_arcs += ok[q];
                 ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
-                hb[q] = ok[q] ? __ldg(a.rp + u[q]) - 1 : 0;
-            }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
                 push[q] = false;
-                if (ok[q]) {
-                    if (ovo[q] >= cu[q]) {
-                        int old = atomicSub(a.histo + hb[q] + cu[q], 1);  // cap bin: cnt
-                        push[q] = (old == cu[q]);                          // exactly once
-                    } else {
-                        red_add(a.histo + hb[q] + ovo[q], -1);
-                    }
-                    red_add(a.histo + hb[q] + cvo[q], 1);
-                }
             }
-            // one aggregated append of all pushes of the U sub-iterations
-            unsigned pm[U];
-            int tot = 0;
 #pragma unroll
-            for (int q = 0; q < U; q++) {
-                pm[q] = __ballot_sync(FULL, push[q]);
-                tot += __popc(pm[q]);
-            }
-            if (tot) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(nF, (unsigned long long)tot);
-                base = __shfl_sync(FULL, base, 0);
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    if (push[q]) a.F[base + __popc(pm[q] & lt_mask)] = u[q];
-                    base += __popc(pm[q]);
-                }
-            }
+            for (int q = 0; q < U; q++)
+                if (ok[q]) push[q] = bin_move(a.histo, __ldg(a.rp + u[q]) - 1, cu[q], cvo[q], ovo[q]);
+            append_pushes<U>(push, u, a.F, nF);
             if (STATS) {
 #pragma unroll
                 for (int q = 0; q < U; q++) {
-                    st_arcs += (j0 + q * 32 + lane) < total;
+                    st_guard += ok[q];
+                    st_push += push[q];
+                }
+            }
+        }
+    }
+    if (STATS) {
+        stat_add(&a.ctl->st_arcs, st_arcs);
+        stat_add(&a.ctl->st_guarded, st_guard);
+        stat_add(&a.ctl->st_pushes, st_push);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// UpdateHisto, pull direction, round t (dense rounds).  Work items: batches
+// of 32 consecutive vertices whose rows are short (deg <= seg; their arcs are
+// one contiguous colidx range) and batches of 32 static hub segments.  A row
+// u is streamed iff core[u] > min core_t(C_t); each arc (u, v) tests v in the
+// changed bitmap and applies the (v, u) bin move to u's own histogram.
+// ---------------------------------------------------------------------------
+template <bool STATS>
+__device__ void pull_phase(const HcArgs &a, int t) {
+    constexpr int U = 4;
+    const int lane = lane_id();
+    const unsigned *chg = a.chg + (t & 1) * a.nwords;
+    const int mincv = ld_volatile(&a.ctl->mincv[t & 1]);
+    const long long nvb = ((long long)a.n + 31) >> 5;
+    const long long nh = (long long)ld_volatile(&a.ctl->nH);
+    const long long nbatch = nvb + ((nh + 31) >> 5);
+    unsigned long long *wc = &a.ctl->wc[t & 1];
+    unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
+    long long st_arcs = 0, st_guard = 0, st_push = 0;
+    const unsigned long long hot = pol_last(), cold = pol_first();
+    for (;;) {
+        long long bidx = 0;
+        if (lane == 0) bidx = (long long)atomicAdd(wc, 1ull);
+        bidx = __shfl_sync(FULL, bidx, 0);
+        if (bidx >= nbatch) break;
+        long long b = 0;
+        int len = 0, cu = 0, uu = 0;
+        if (bidx < nvb) {
+            long long v = bidx * 32 + lane;
+            if (v < a.n) {
+                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+                uu = (int)v;
+                if (r1 > r0 && r1 - r0 <= a.tn.seg) {
+                    cu = core_of(a, uu, hot);
+                    if (cu > mincv) { b = r0; len = (int)(r1 - r0); }
+                }
+            }
+        } else {
+            long long i = (bidx - nvb) * 32 + lane;
+            if (i < nh) {
+                int2 sg = ld_stream_int2(a.H + i, cold);
+                uu = sg.x;
+                cu = core_of(a, uu, hot);
+                if (cu > mincv) {
+                    long long r0 = __ldg(a.rp + uu), r1 = __ldg(a.rp + uu + 1);
+                    b = r0 + (long long)sg.y * a.tn.seg;
+                    len = (int)min((long long)a.tn.seg, r1 - b);
+                }
+            }
+        }
+        long long hbu = len ? __ldg(a.rp + uu) - 1 : 0;
+        int incl = warp_incl_scan(len);
+        int excl = incl - len;
+        int total = __shfl_sync(FULL, incl, 31);
+        for (int j0 = 0; j0 < total; j0 += 32 * U) {
+            int v[U], cuo[U], uo[U], cv[U];
+            long long hbo[U];
+            bool ok[U], push[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                int j = j0 + q * 32 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    int cand = lo + step;
+                    int ex = __shfl_sync(FULL, excl, cand & 31);
+                    if (cand < 32 && ex <= j) lo = cand;
+                }
+                long long eb = __shfl_sync(FULL, b, lo);
+                int ex = __shfl_sync(FULL, excl, lo);
+                cuo[q] = __shfl_sync(FULL, cu, lo);
+                uo[q] = __shfl_sync(FULL, uu, lo);
+                hbo[q] = __shfl_sync(FULL, hbu, lo);
+                ok[q] = j < total;
+                v[q] = ok[q] ? ld_stream(a.ci + eb + (j - ex), cold) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                if (STATS) st_arcs += ok[q];
+                ok[q] = ok[q] && ((ld_cg_u32(chg + (v[q] >> 5), hot) >> (v[q] & 31)) & 1u);
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                cv[q] = ok[q] ? core_of(a, v[q], hot) : 0;
+                ok[q] = ok[q] && cv[q] < cuo[q];
+                push[q] = false;
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++)
+                if (ok[q]) push[q] = bin_move(a.histo, hbo[q], cuo[q], cv[q], __ldcg(a.oldc + v[q]));
+            append_pushes<U>(push, uo, a.F, nF);
+            if (STATS) {
+#pragma unroll
+                for (int q = 0; q < U; q++) {
                     st_guard += ok[q];
                     st_push += push[q];
                 }
@@ -445,6 +664,7 @@ __device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long n
     unsigned long long *nS = &a.ctl->nS[t & 1];
     long long iters = (nf + nthreads - 1) / nthreads;
     long long st_bins = 0;
+    ChangeAcc acc;
     for (long long it = 0; it < iters; it++) {
         long long i = it * nthreads + gthread;
         bool valid = i < nf;
@@ -454,8 +674,8 @@ __device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long n
         if (valid) {
             v = __ldcg(a.F + i);
             cold = __ldcg(a.core + v);
-            hb = a.rp[v] - 1;  // bin b at hb + b
-            d = a.rp[v + 1] - hb - 1;
+            hb = __ldg(a.rp + v) - 1;  // bin b at hb + b
+            d = __ldg(a.rp + v + 1) - hb - 1;
             k = cold;
             done = false;
             for (int stp = 0; stp < 32; stp++) {
@@ -494,32 +714,53 @@ __device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long n
         int nseg = 0;
         if (valid) {
             a.core[v] = k;
+            set_c8(a, v, k);
             a.oldc[v] = cold;
             a.histo[hb + k] = sum;  // cap bin := cnt
             nseg = nseg_of(d, a.tn.seg);
         }
+        if (valid) acc.note(a, t, v, k, d);
         warp_append_segments(v, nseg, a.S, nS);
     }
+    acc.flush(a, t, nullptr);
     if (STATS) stat_add(&a.ctl->st_bins, st_bins);
+}
+
+// start-of-UpdateHisto(t) bookkeeping: reset round t+1's counters (unused
+// during this phase), clear round t+1's bitmap, pick push or pull
+__device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool leader, long long gthread,
+                                                long long nthreads, bool stats) {
+    if (leader) {
+        a.ctl->nS[(t + 1) & 1] = 0;
+        a.ctl->wc[(t + 1) & 1] = 0;
+        a.ctl->arcsC[(t + 1) & 1] = 0;
+        a.ctl->mincv[(t + 1) & 1] = INT_MAX;
+        if (stats) a.ctl->st_segs += ld_volatile(&a.ctl->nS[t & 1]);
+    }
+    unsigned *clr = a.chg + ((t + 1) & 1) * a.nwords;
+    for (long long w = gthread; w < a.nwords; w += nthreads) clr[w] = 0u;
+    unsigned long long ac = ld_volatile(&a.ctl->arcsC[t & 1]);
+    if (leader && (unsigned long long)t < a.fsz_cap) a.rarcs[t] = ac;
+    return a.allow_pull && ac * (unsigned long long)a.tn.pull_div >= (unsigned long long)a.arcs;
 }
 
 // ---------------------------------------------------------------------------
 // persistent cooperative kernel: all rounds t >= 1 with grid barriers
 // ---------------------------------------------------------------------------
 template <bool STATS>
-__global__ void __launch_bounds__(512) hc_rounds_kernel(HcArgs a) {
+__global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
-    const long long gwarp = gthread >> 5, nwarps = nthreads >> 5;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     if (ld_volatile(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
     for (int t = 1;; t++) {
-        if (leader) {
-            a.ctl->nS[(t + 1) & 1] = 0;
-            a.ctl->wc[(t + 1) & 1] = 0;
-            if (STATS) a.ctl->st_segs += ld_volatile(&a.ctl->nS[t & 1]);
+        bool pull = update_prologue(a, t, leader, gthread, nthreads, STATS);
+        if (pull) {
+            if (STATS && leader) a.ctl->st_pull++;
+            pull_phase<STATS>(a, t);
+        } else {
+            update_phase<STATS>(a, t);
         }
-        update_phase<STATS>(a, t);
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
         unsigned long long nf = ld_volatile(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
@@ -536,25 +777,24 @@ __global__ void __launch_bounds__(512) hc_rounds_kernel(HcArgs a) {
 
 // host-loop variants (PICO_F_HOST_LOOP): one launch per phase
 template <bool STATS>
-__global__ void __launch_bounds__(512) hc_update_kernel(HcArgs a, int t) {
+__global__ void __launch_bounds__(512, 2) hc_update_kernel(HcArgs a, int t, int pull) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.ctl->nS[(t + 1) & 1] = 0;
-        a.ctl->wc[(t + 1) & 1] = 0;
-        if (STATS) a.ctl->st_segs += a.ctl->nS[t & 1];
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    update_prologue(a, t, leader, gthread, nthreads, STATS);
+    if (pull) {
+        if (STATS && leader) a.ctl->st_pull++;
+        pull_phase<STATS>(a, t);
+    } else {
+        update_phase<STATS>(a, t);
     }
-    update_phase<STATS>(a, t);
 }
 
 template <bool STATS>
 __global__ void __launch_bounds__(512) hc_sum_kernel(HcArgs a, int t) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.ctl->nF[(t + 1) & 1] = 0;
-        a.ctl->rounds++;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->nF[(t + 1) & 1] = 0;
     sum_phase<STATS>(a, t, gthread, nthreads);
 }
 
@@ -570,18 +810,40 @@ Tune hc_tune(uint32_t flags) {
     } else {
         t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = 256;
     }
+    t.pull_div = 8;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
+    if (flags & PICO_F_PULL_ALWAYS) t.pull_div = 1 << 30;
     return t;
 }
 
-size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags) {
+struct HcLayout {
+    size_t ctl, fsz, rarcs, histo, c8, oldc, F, BC, S, H, chg, total;
+    long long nwords, scap, hcap;
+};
+
+static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     Tune tn = hc_tune(flags);
+    HcLayout L;
+    L.nwords = (n + 31) / 32;
+    L.scap = n + arcs / tn.seg + 64;
+    L.hcap = 2 * (arcs / tn.seg) + 64;
     size_t b = 0;
-    b += align256(sizeof(Ctrl));
-    b += align256(sizeof(unsigned long long) * kFszCap);
-    b += align256(sizeof(int) * (size_t)arcs);             // histo
-    b += align256(sizeof(int) * (size_t)n) * 3;           // oldc, F, BC
-    b += align256(sizeof(int2) * (size_t)(n + arcs / tn.seg + 64));  // S
-    return b;
+    L.ctl = b; b += align256(sizeof(Ctrl));
+    L.fsz = b; b += align256(sizeof(unsigned long long) * kFszCap);
+    L.rarcs = b; b += align256(sizeof(unsigned long long) * kFszCap);
+    L.histo = b; b += align256(sizeof(int) * (size_t)arcs);
+    L.c8 = b; b += align256(sizeof(shadow_t) * (size_t)n);
+    L.oldc = b; b += align256(sizeof(int) * (size_t)n);
+    L.F = b; b += align256(sizeof(int) * (size_t)n);
+    L.BC = b; b += align256(sizeof(int) * (size_t)n);
+    L.S = b; b += align256(sizeof(int2) * (size_t)L.scap);
+    L.H = b; b += align256(sizeof(int2) * (size_t)L.hcap);
+    L.chg = b; b += align256(sizeof(unsigned) * 2 * (size_t)L.nwords);
+    L.total = b;
+    return L;
+}
+
+size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags) {
+    return hc_layout(n, arcs, flags).total;
 }
 
 struct Timer {
@@ -622,27 +884,39 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                             pico_stats_t *st, const DevInfo &dev) {
     HcArgs a;
     Tune tn = hc_tune(flags);
+    HcLayout L = hc_layout(n, arcs, flags);
     char *p = (char *)ws;
-    a.ctl = (Ctrl *)p; p += align256(sizeof(Ctrl));
-    a.fsz = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * kFszCap);
+    a.ctl = (Ctrl *)(p + L.ctl);
+    a.fsz = (unsigned long long *)(p + L.fsz);
+    a.rarcs = (unsigned long long *)(p + L.rarcs);
     a.fsz_cap = kFszCap;
-    a.histo = (int *)p; p += align256(sizeof(int) * (size_t)arcs);
-    a.oldc = (int *)p; p += align256(sizeof(int) * (size_t)n);
-    a.F = (int *)p; p += align256(sizeof(int) * (size_t)n);
-    a.BC = (int *)p; p += align256(sizeof(int) * (size_t)n);
-    a.S = (int2 *)p;
-    a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core; a.tn = tn;
+    a.histo = (int *)(p + L.histo);
+    a.c8 = (shadow_t *)(p + L.c8);
+    a.oldc = (int *)(p + L.oldc);
+    a.F = (int *)(p + L.F);
+    a.BC = (int *)(p + L.BC);
+    a.S = (int2 *)(p + L.S);
+    a.H = (int2 *)(p + L.H);
+    a.chg = (unsigned *)(p + L.chg);
+    a.nwords = L.nwords;
+    a.rp = rp; a.ci = ci; a.n = (int)n; a.arcs = arcs; a.core = core; a.tn = tn;
+    a.allow_pull = (flags & PICO_F_PUSH_ONLY) ? 0 : 1;
 
     Timer tm{s, (flags & PICO_F_TIMING) != 0, {}};
     cudaError_t err;
-    if ((err = cudaMemsetAsync(a.ctl, 0, sizeof(Ctrl), s))) return err;
+    Ctrl hc{};
+    hc.mincv[0] = hc.mincv[1] = INT_MAX;
+    if ((err = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
+    if ((err = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)L.nwords, s))) return err;
 
     const int sms = dev.sms;
+    long long launches = 0;
     // H0
     tm.start(PICO_K_DEGREE);
     {
         int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 16);
         hc_degree_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+        launches++;
     }
     tm.stop();
     // H1-H3 (round 1)
@@ -659,11 +933,13 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                              (int)smC);
         hc_init_cta_kernel<STATS><<<sms, 512, smC, s>>>(a);
         hc_init_fallback_kernel<STATS><<<sms, 512, 0, s>>>(a);
+        int nb = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
+        hc_shadow_kernel<<<std::max(nb, 1), 256, 0, s>>>(a);
+        launches += 5;
     }
     tm.stop();
     if ((err = cudaGetLastError())) return err;
 
-    long long launches = 5;  // degree + 4 init kernels
     unsigned long long c1 = 0, s1 = 0;
     if ((err = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return err;
     if ((err = cudaMemcpyAsync(&s1, &a.ctl->nS[1], sizeof(s1), cudaMemcpyDeviceToHost, s))) return err;
@@ -675,12 +951,19 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     // counters as the rounds expect them: nF[1] held |C_1|, F list empty
     if ((err = cudaMemsetAsync(&a.ctl->nF[1], 0, sizeof(unsigned long long), s))) return err;
 
+    std::vector<unsigned long long> harcs;
     if (c1) {
         if (flags & PICO_F_HOST_LOOP) {
             int blocks = sms * 4;
             for (int t = 1;; t++) {
+                unsigned long long ac = 0;
+                if ((err = cudaMemcpyAsync(&ac, &a.ctl->arcsC[t & 1], sizeof(ac), cudaMemcpyDeviceToHost, s)))
+                    return err;
+                if ((err = cudaStreamSynchronize(s))) return err;
+                harcs.push_back(ac);
+                int pull = a.allow_pull && ac * (unsigned long long)tn.pull_div >= (unsigned long long)arcs;
                 tm.start(PICO_K_UPDATE);
-                hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t);
+                hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t, pull);
                 tm.stop();
                 launches++;
                 unsigned long long nf = 0;
@@ -697,12 +980,6 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 tm.stop();
                 launches++;
             }
-            if (STATS) {
-                unsigned long long tot = 0;
-                for (auto x : hsz) tot += x;
-                // frontier_total filled below from hsz
-                (void)tot;
-            }
         } else {
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hc_rounds_kernel<STATS>, 512, 0);
@@ -718,14 +995,19 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
             if ((err = cudaMemcpyAsync(&devrounds, &a.ctl->rounds, sizeof(devrounds),
                                        cudaMemcpyDeviceToHost, s)))
                 return err;
-            std::vector<unsigned long long> dsz(std::min<unsigned long long>(devrounds + 1, kFszCap), 0);
-            if (!dsz.empty() &&
-                (err = cudaMemcpyAsync(dsz.data(), a.fsz, sizeof(unsigned long long) * dsz.size(),
+            if ((err = cudaStreamSynchronize(s))) return err;
+            size_t nr = (size_t)std::min<unsigned long long>(devrounds + 2, kFszCap);
+            std::vector<unsigned long long> dsz(nr, 0), dar(nr, 0);
+            if ((err = cudaMemcpyAsync(dsz.data(), a.fsz, sizeof(unsigned long long) * nr,
+                                       cudaMemcpyDeviceToHost, s)))
+                return err;
+            if ((err = cudaMemcpyAsync(dar.data(), a.rarcs, sizeof(unsigned long long) * nr,
                                        cudaMemcpyDeviceToHost, s)))
                 return err;
             if ((err = cudaStreamSynchronize(s))) return err;
             rounds += devrounds;
             for (unsigned long long t = 1; t <= devrounds && t < kFszCap; t++) hsz.push_back(dsz[t]);
+            for (unsigned long long t = 1; t <= devrounds + 1 && t < nr; t++) harcs.push_back(dar[t]);
         }
     }
     if ((err = cudaGetLastError())) return err;
@@ -736,6 +1018,9 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         if (st->frontier_sizes)
             for (size_t i = 0; i < hsz.size() && (int64_t)i < st->frontier_sizes_cap; i++)
                 st->frontier_sizes[i] = (int64_t)hsz[i];
+        if (st->round_arcs)
+            for (size_t i = 0; i < harcs.size() && (int64_t)i < st->frontier_sizes_cap; i++)
+                st->round_arcs[i] = (int64_t)harcs[i];
         if (STATS) {
             Ctrl h;
             if ((err = cudaMemcpyAsync(&h, a.ctl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s))) return err;
@@ -749,7 +1034,8 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
             st->bins_read = (int64_t)h.st_bins;
             st->pushes = (int64_t)h.st_pushes;
             st->hub_fallbacks = (int64_t)h.st_fallback;
-            st->segments = (int64_t)(h.st_segs + (c1 ? 0 : 0));
+            st->segments = (int64_t)h.st_segs;
+            st->pull_rounds = (int64_t)h.st_pull;
         }
     }
     tm.collect(st);

@@ -67,8 +67,8 @@ def test_host_side_argument_errors(lib):
 
 
 def test_stats_struct_layout():
-    # pico_stats_t: 15 int64 + double[8] + int64[8] + pointer + int64
-    assert ctypes.sizeof(_lib.Stats) == 15 * 8 + 8 * 8 + 8 * 8 + 8 + 8
+    # pico_stats_t: 16 int64 + double[8] + int64[8] + pointer + int64 + pointer
+    assert ctypes.sizeof(_lib.Stats) == 16 * 8 + 8 * 8 + 8 * 8 + 8 + 8 + 8
 
 
 def test_python_api_refuses_cpu_tensors(lib):

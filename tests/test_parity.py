@@ -21,7 +21,11 @@ def _pico():
 
 def _variants(algo):
     pico = _pico()
-    base = [0, pico.F_HOST_LOOP, pico.F_TINY_TILES, pico.F_TINY_TILES | pico.F_HOST_LOOP, pico.F_STATS]
+    base = [0, pico.F_HOST_LOOP, pico.F_TINY_TILES, pico.F_TINY_TILES | pico.F_HOST_LOOP, pico.F_STATS,
+            pico.F_RELABEL, pico.F_RELABEL | pico.F_TINY_TILES | pico.F_STATS]
+    if algo == "histocore":
+        base += [pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
+                 pico.F_PULL_ALWAYS | pico.F_HOST_LOOP, pico.F_PUSH_ONLY | pico.F_HOST_LOOP]
     if algo == "peelone":
         base += [pico.F_CLAMP_SUB, pico.F_CLAMP_SUB | pico.F_HOST_LOOP, pico.F_CLAMP_SUB | pico.F_TINY_TILES]
     return base
@@ -164,7 +168,7 @@ def test_c1_rmat16_full():
     ref = oracle.bz(rp, ci)
     jac = oracle.jacobi_rounds(rp, ci)
     for algo in ALGOS:
-        for fl in (0, _pico().F_HOST_LOOP, _pico().F_STATS):
+        for fl in (0, _pico().F_HOST_LOOP, _pico().F_STATS, _pico().F_RELABEL):
             _check(rp, ci, algo, fl, ref, jac)
     assert oracle.kcore_check(rp, ci, ref)
 
