@@ -80,7 +80,10 @@ enum {
     PICO_F_TIMING = 4u,       /* per-kernel device time via CUDA events      */
     PICO_F_HOST_LOOP = 8u,    /* one kernel launch per phase, host-driven    */
     PICO_F_CLAMP_SUB = 16u,   /* PeelOne: atomicSub + end-of-level repair    */
-                              /* instead of the CAS clamp  */
+                              /* (SURVEY 8(c)#18b); default is atomicSub +   */
+                              /* atomicMax(k) on overshoot                   */
+    PICO_F_CLAMP_CAS = 1024u, /* PeelOne: CAS-loop atomicSub>=k (the literal */
+                              /* single-transaction clamp of P:273)          */
     PICO_F_TINY_TILES = 32u,  /* test-only: tiny degree-class thresholds and */
                               /* shared-memory bin caps so every code path   */
                               /* (incl. the global-histogram fallback) runs  */
@@ -116,7 +119,8 @@ typedef struct {
     /* iteration counts */
     int64_t rounds;         /* HistoCore l2: rounds with a non-empty frontier */
     int64_t levels;         /* PeelOne: non-empty levels (= #distinct cores)  */
-    int64_t subrounds;      /* PeelOne: levels actually scanned               */
+    int64_t subrounds;      /* PeelOne: bulk-synchronous sub-rounds that      */
+                            /* drained the dynamic frontiers of all levels   */
     int64_t kmax;           /* max coreness                                   */
     /* work counters (PICO_F_STATS), the terms of DESIGN.md "algorithmic bytes" */
     int64_t frontier_total;     /* HistoCore: sum_t |F_t| incl. round 1        */

@@ -148,6 +148,31 @@ __device__ __forceinline__ void grid_barrier(unsigned *arrive, unsigned *gen) {
     __syncthreads();
 }
 
+// Grid barrier that also publishes a consistent snapshot: the last CTA to
+// arrive (all other CTAs' writes are fenced by then) copies *src to *dst
+// before releasing the barrier.
+__device__ __forceinline__ void grid_barrier_snap(unsigned *arrive, unsigned *gen,
+                                                  const unsigned long long *src,
+                                                  unsigned long long *dst) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g = *reinterpret_cast<volatile unsigned *>(gen);
+        __threadfence();
+        unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(arrive, 1u) == nb - 1) {
+            *reinterpret_cast<volatile unsigned long long *>(dst) =
+                *reinterpret_cast<const volatile unsigned long long *>(src);
+            *reinterpret_cast<volatile unsigned *>(arrive) = 0;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned *>(gen) == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // Workspace control block (device memory, initialised at the start of a call).
 struct Ctrl {
     // HistoCore lists: F (frontier vertex ids) and S (update segments),
@@ -167,7 +192,7 @@ struct Ctrl {
     alignas(128) unsigned long long q_head;     // next queue slot to claim
     alignas(128) unsigned long long q_tail;     // next queue slot to write
     alignas(128) unsigned long long q_pending;  // pushed, not fully processed
-    alignas(128) unsigned long long q_pad;
+    alignas(128) unsigned long long q_snap;     // tail snapshot at the last barrier
     unsigned long long nAlive[2];  // alive list lengths (ping-pong by level)
     unsigned long long nProc[2];   // vertices processed per level (parity)
     unsigned long long levels;     // non-empty levels

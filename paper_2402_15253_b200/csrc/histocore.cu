@@ -478,10 +478,17 @@ __device__ void update_phase(const HcArgs &a, int t) {
     unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
     long long st_arcs = 0, st_guard = 0, st_push = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
-    for (;;) {
-        long long bidx = 0;
-        if (lane == 0) bidx = (long long)atomicAdd(wc, 1ull);
-        bidx = __shfl_sync(FULL, bidx, 0);
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long round = 0;; round++) {
+        // first batch static (warp id), the rest claimed dynamically (one
+        // atomic per 32 work items); small rounds cost no claim atomics
+        long long bidx = gwarp;
+        if (round > 0) {
+            if (nbatch <= nwarps) break;
+            if (lane == 0) bidx = nwarps + (long long)atomicAdd(wc, 1ull);
+            bidx = __shfl_sync(FULL, bidx, 0);
+        }
         if (bidx >= nbatch) break;
         long long i = bidx * 32 + lane;
         long long b = 0;
@@ -565,10 +572,17 @@ __device__ void pull_phase(const HcArgs &a, int t) {
     unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
     long long st_arcs = 0, st_guard = 0, st_push = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
-    for (;;) {
-        long long bidx = 0;
-        if (lane == 0) bidx = (long long)atomicAdd(wc, 1ull);
-        bidx = __shfl_sync(FULL, bidx, 0);
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long round = 0;; round++) {
+        // first batch static (warp id), the rest claimed dynamically (one
+        // atomic per 32 work items); small rounds cost no claim atomics
+        long long bidx = gwarp;
+        if (round > 0) {
+            if (nbatch <= nwarps) break;
+            if (lane == 0) bidx = nwarps + (long long)atomicAdd(wc, 1ull);
+            bidx = __shfl_sync(FULL, bidx, 0);
+        }
         if (bidx >= nbatch) break;
         long long b = 0;
         int len = 0, cu = 0, uu = 0;

@@ -11,22 +11,24 @@
 //                                                         (dynamic frontier P:342;
 //                                                          SURVEY 8(c)#19)
 // The level index k jumps to a lower bound of the minimum alive core, so only
-// non-empty levels (plus at most the final one) are scanned; the level count
-// is k_max's number of distinct coreness values (l1 = k_max).
+// non-empty levels (plus at most the final one) are scanned; the number of
+// non-empty levels is the number of distinct coreness values (l1 =
+// k_max).
 //
-// B200 design: one persistent cooperative kernel runs every level (two grid
-// barriers per level, no host round trips).  The scan walks a compacted alive
-// list (ping-pong), never all n vertices.  Each level's queue is drained by
-// all warps through a run-wide log Q of (vertex, segment) entries (every
-// vertex is processed exactly once over the run, so Q never wraps): warps
-// claim up to 32 entries with one CAS, walk the rows with warp-level load
-// balancing, and push newly clamped vertices back into Q.  A `pending`
-// counter (entries pushed but not finished) detects the end of a level.
+// B200 design: one persistent cooperative kernel runs every level.  The scan
+// walks a compacted alive list (ping-pong), never all n vertices.  The level's
+// queue lives in a run-wide log Q of (vertex, segment) entries (every vertex
+// is processed exactly once over the run, so Q never wraps; hub rows are split
+// into 256-arc entries).  The dynamic frontier is drained in bulk-synchronous
+// sub-rounds: sub-round r processes the entries appended by sub-round r-1,
+// warps claim batches of 32 entries with one atomicAdd (no CAS, no polling),
+// walk the rows with warp-level load balancing and append newly clamped
+// vertices at the tail; one grid barrier per sub-round, whose last arriving
+// CTA publishes a consistent snapshot of the tail.
 //
-// Two bit-exact implementations of atomicSub>=k:
-//   CAS loop (default): read-compute-CAS, never below k (faithful to P:273).
-//   CLAMP_SUB (PICO_F_CLAMP_SUB): atomicSub, push on old == k+1, and an
-//     end-of-level repair core[v] = k over the level's queue range.
+// Three bit-exact implementations of atomicSub>=k, see
+// clamp_dec(): atomicSub + atomicMax on overshoot (default), atomicSub + end-
+// of-level repair (PICO_F_CLAMP_SUB), CAS loop (PICO_F_CLAMP_CAS).
 #include <climits>
 
 #include "common.cuh"
@@ -41,7 +43,7 @@ struct PoArgs {
     int *core;
     int *alive0;
     int *alive1;
-    long long *Q;  // (v << 32) | segment, -1 = not yet written
+    long long *Q;  // (v << 32) | segment
     unsigned long long *fsz;
     unsigned long long fsz_cap;
     Ctrl *ctl;
@@ -50,8 +52,8 @@ struct PoArgs {
 
 __device__ __forceinline__ int po_nseg(long long d, int seg) { return (int)((d + seg - 1) / seg); }
 
-// Warp-cooperative push of vertices (pred lanes) into the queue, one entry per
-// `seg` arcs.  Lane 0 performs all pending/tail atomics (program order).
+// Warp-cooperative append of vertices (pred lanes) to the queue tail, one entry
+// per `seg` arcs of the row.  Returns the number of vertices appended.
 __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     const int lane = lane_id();
     int ns = 0;
@@ -60,14 +62,10 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return 0;
     unsigned long long base = 0;
-    if (lane == 0) {
-        atomicAdd(&a.ctl->q_pending, (unsigned long long)total);
-        base = atomicAdd(&a.ctl->q_tail, (unsigned long long)total);
-    }
+    if (lane == 0) base = atomicAdd(&a.ctl->q_tail, (unsigned long long)total);
     base = __shfl_sync(FULL, base, 0);
     unsigned long long off = base + (unsigned long long)(incl - ns);
-    for (int s = 0; s < ns; s++)
-        *reinterpret_cast<volatile long long *>(a.Q + off + s) = ((long long)v << 32) | s;
+    for (int s = 0; s < ns; s++) a.Q[off + s] = ((long long)v << 32) | s;
     return __popc(__ballot_sync(FULL, pred));
 }
 
@@ -95,123 +93,85 @@ __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, 
         nproc += po_push(a, front, v);
     }
     kmin = warp_min(kmin);
+    // po_push returns the warp-wide count to every lane: lane 0 holds the total
     if (lane_id() == 0) {
         if (kmin != INT_MAX) atomicMin(&a.ctl->kminb[p ^ 1], kmin);
         if (nproc) atomicAdd(&a.ctl->nProc[p], (unsigned long long)nproc);
-        if (STATS) atomicAdd(&a.ctl->st_alive, (unsigned long long)(gthread == 0 ? na : 0));
+        if (STATS && gthread == 0) atomicAdd(&a.ctl->st_alive, (unsigned long long)na);
     }
 }
 
-// drain of level k: process queue entries until none is pending.  One thread
-// per CTA polls and claims a chunk of entries (CAS on the head); the CTA's
-// warps split the chunk 32 entries each and walk the rows with warp-level
-// load balancing; newly clamped vertices are pushed back into the queue.
-template <bool CLAMP_SUB, bool STATS>
-__device__ void po_drain_phase(const PoArgs &a, int k, int p) {
-    __shared__ unsigned long long s_base;
-    __shared__ int s_got;
-    const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// clamped decrement atomicSub>=k(core[u], 1, k) of P:273; returns the old
+// value (> k: the caller decremented; == k+1: it set the value to k).
+//   MODE 0 (default): atomicSub, and only if that overshot below k an
+//     atomicMax(k) -- exact, at most two atomics, no retry loop under the
+//     contention of hub vertices; every value is >= k again before the level's
+//     closing barrier (all readers of transient values skip them: guard c > k).
+//   MODE 1 (PICO_F_CLAMP_SUB): atomicSub only; the level's queue range is
+//     repaired to k after the level (SURVEY 8(c)#18 b).
+//   MODE 2 (PICO_F_CLAMP_CAS): compare-and-swap loop, never below k (the
+//     literal "single atomic transaction", SURVEY 8(c)#18 a).
+template <int MODE>
+__device__ __forceinline__ int clamp_dec(int *p, int c, int k) {
+    if (MODE == 2) {
+        int old = c;
+        for (;;) {
+            if (old <= k) return old;
+            int prev = atomicCAS(p, old, old - 1);
+            if (prev == old) return old;
+            old = prev;
+        }
+    }
+    int old = atomicSub(p, 1);
+    if (MODE == 0 && old <= k) atomicMax(p, k);
+    return old;
+}
+
+// one sub-round of level k: process queue entries [lo, hi).  Entries hold at
+// most `seg` (<= 32) arcs, so one warp takes one entry per iteration (lanes =
+// arcs, one gather + one clamp in flight per lane): a sub-round's latency is a
+// single memory round trip per entry instead of a serial walk of long rows.
+template <int MODE, bool STATS>
+__device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long lo, unsigned long long hi) {
+    const int lane = lane_id();
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     int kmin = INT_MAX;
     long long nproc = 0, st_arcs = 0, st_dec = 0;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            unsigned long long base = 0;
-            int got = 0;
-            for (int spin = 0;; spin++) {
-                unsigned long long h = ld_volatile(&a.ctl->q_head);
-                unsigned long long t = ld_volatile(&a.ctl->q_tail);
-                if (h < t) {
-                    unsigned long long avail = t - h;
-                    unsigned long long share = (avail + gridDim.x - 1) / gridDim.x;
-                    unsigned long long want = min(avail, max(32ull, min((unsigned long long)(32 * nw), share)));
-                    if (atomicCAS(&a.ctl->q_head, h, h + want) == h) {
-                        base = h;
-                        got = (int)want;
-                        break;
-                    }
-                } else {
-                    if (ld_volatile(&a.ctl->q_pending) == 0) break;
-                    __nanosleep(min(1024, 32 << min(spin, 5)));
-                }
-            }
-            s_base = base;
-            s_got = got;
-        }
-        __syncthreads();
-        const int got = s_got;
-        const unsigned long long base = s_base;
-        __syncthreads();
-        if (got == 0) break;
-        const int myn = min(32, got - wid * 32);
-        if (myn > 0) {
-            long long b = 0;
-            int len = 0;
-            if (lane < myn) {
-                long long e;
-                do {
-                    e = *reinterpret_cast<volatile long long *>(a.Q + base + wid * 32 + lane);
-                } while (e < 0);
-                int v = (int)(e >> 32);
-                int s = (int)(e & 0xffffffffll);
-                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-                b = r0 + (long long)s * a.seg;
-                len = (int)min((long long)a.seg, r1 - b);
-            }
-            int incl = warp_incl_scan(len);
-            int excl = incl - len;
-            int total = __shfl_sync(FULL, incl, 31);
-            for (int j0 = 0; j0 < total; j0 += 32) {
-                int j = j0 + lane;
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step >= 1; step >>= 1) {
-                    int cand = lo + step;
-                    int ex = __shfl_sync(FULL, excl, cand & 31);
-                    if (cand < 32 && ex <= j) lo = cand;
-                }
-                long long eb = __shfl_sync(FULL, b, lo);
-                int ex = __shfl_sync(FULL, excl, lo);
-                bool push = false;
-                int u = 0;
-                if (j < total) {
-                    u = __ldg(a.ci + eb + (j - ex));
-                    int c = __ldcg(a.core + u);
-                    if (STATS) st_arcs++;
-                    if (c > k) {  // guard core[u] > k
-                        int old;
-                        if (CLAMP_SUB) {
-                            old = atomicSub(a.core + u, 1);
-                        } else {
-                            old = c;
-                            for (;;) {  // atomicSub>=k as a CAS loop
-                                if (old <= k) break;
-                                int prev = atomicCAS(a.core + u, old, old - 1);
-                                if (prev == old) break;
-                                old = prev;
-                            }
-                        }
-                        if (STATS) st_dec++;
-                        push = (old == k + 1);
-                        if (old - 1 > k) kmin = min(kmin, old - 1);
-                    }
-                }
-                nproc += po_push(a, push, u);
+    for (unsigned long long i = lo + gwarp; i < hi; i += nwarps) {
+        long long e = __ldcg(a.Q + i);
+        int v = (int)(e >> 32);
+        int s = (int)(e & 0xffffffffll);
+        long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+        long long b = r0 + (long long)s * a.seg;
+        int len = (int)min((long long)a.seg, r1 - b);
+        bool push = false;
+        int u = 0;
+        if (lane < len) {
+            u = __ldg(a.ci + b + lane);
+            int c = __ldcg(a.core + u);
+            if (STATS) st_arcs++;
+            if (c > k) {  // guard core[u] > k
+                int old = clamp_dec<MODE>(a.core + u, c, k);
+                if (STATS) st_dec += (old > k);
+                push = (old == k + 1);
+                if (old - 1 > k) kmin = min(kmin, old - 1);
             }
         }
-        __syncthreads();  // all pushes of this chunk precede its release
-        if (threadIdx.x == 0) atomicAdd(&a.ctl->q_pending, 0ull - (unsigned long long)got);
+        nproc += po_push(a, push, u);
     }
     kmin = warp_min(kmin);
+    // po_push returns the warp-wide count to every lane: lane 0 holds the total
     if (lane == 0) {
         if (kmin != INT_MAX) atomicMin(&a.ctl->kminb[p ^ 1], kmin);
         if (nproc) atomicAdd(&a.ctl->nProc[p], (unsigned long long)nproc);
     }
     if (STATS) {
-        long long s1 = warp_sum64(st_arcs), s2 = warp_sum64(st_dec), s3 = warp_sum64(nproc);
+        long long s1 = warp_sum64(st_arcs), s2 = warp_sum64(st_dec);
         if (lane == 0) {
             if (s1) atomicAdd(&a.ctl->st_arcs, (unsigned long long)s1);
             if (s2) atomicAdd(&a.ctl->st_guarded, (unsigned long long)s2);
-            if (s3) atomicAdd(&a.ctl->st_pushes, (unsigned long long)s3);
+            if (nproc) atomicAdd(&a.ctl->st_pushes, (unsigned long long)nproc);
         }
     }
 }
@@ -260,34 +220,42 @@ __global__ void po_init_kernel(PoArgs a) {
 // ---------------------------------------------------------------------------
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
-template <bool CLAMP_SUB, bool STATS>
+template <int MODE, bool STATS>
 __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
+    constexpr bool CLAMP_SUB = MODE == 1;
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    Ctrl *c = a.ctl;
     int k = 0, kprev = 0;
-    unsigned long long lstart = 0;
-    int L = 0;
-    for (;; L++) {
+    unsigned long long S = 0;  // global sub-round counter (claim counter parity)
+    for (int L = 0;; L++) {
         const int p = L & 1;
-        long long na = (long long)ld_volatile(&a.ctl->nAlive[p]);
+        long long na = (long long)ld_volatile(&c->nAlive[p]);
         if (leader && L > 0) po_close_level(a, p ^ 1, kprev);
         if (na == 0) break;
-        k = max(k + 1, ld_volatile(&a.ctl->kminb[p]));
+        k = max(k + 1, ld_volatile(&c->kminb[p]));
+        unsigned long long lstart = ld_volatile(&c->q_snap);
         po_scan_phase<STATS>(a, k, p, gthread, nthreads);
-        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
         if (leader) {
-            a.ctl->nAlive[p] = 0;        // alive[p] consumed; refilled at level L+1
-            a.ctl->kminb[p] = INT_MAX;   // consumed at this level's head
+            c->nAlive[p] = 0;       // alive[p] consumed; refilled at level L+1
+            c->kminb[p] = INT_MAX;  // consumed at this level's head
         }
-        po_drain_phase<CLAMP_SUB, STATS>(a, k, p);
-        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        unsigned long long lo = lstart;
+        for (;;) {
+            unsigned long long hi = ld_volatile(&c->q_snap);
+            if (hi == lo) break;  // uniform: every CTA read the same snapshot
+            po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
+            grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
+            lo = hi;
+            S++;
+        }
         if (CLAMP_SUB) {
-            unsigned long long lend = ld_volatile(&a.ctl->q_tail);
-            po_repair_phase(a, k, lstart, lend, gthread, nthreads);
-            lstart = lend;
-            grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+            po_repair_phase(a, k, lstart, lo, gthread, nthreads);
+            grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
         }
+        if (leader) c->rounds = S;  // BSP sub-rounds so far
         kprev = k;
     }
 }
@@ -300,13 +268,14 @@ __global__ void __launch_bounds__(512) po_scan_kernel(PoArgs a, int k, int p) {
     po_scan_phase<STATS>(a, k, p, gthread, nthreads);
 }
 
-template <bool CLAMP_SUB, bool STATS>
-__global__ void __launch_bounds__(512) po_drain_kernel(PoArgs a, int k, int p) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+template <int MODE, bool STATS>
+__global__ void __launch_bounds__(512) po_sub_kernel(PoArgs a, int k, int p, unsigned long long lo,
+                                                     unsigned long long hi, int first) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && first) {
         a.ctl->nAlive[p] = 0;
         a.ctl->kminb[p] = INT_MAX;
     }
-    po_drain_phase<CLAMP_SUB, STATS>(a, k, p);
+    po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
 }
 
 __global__ void po_repair_kernel(PoArgs a, int k, unsigned long long lo, unsigned long long hi) {
@@ -321,7 +290,7 @@ __global__ void po_close_kernel(PoArgs a, int p, int k) { po_close_level(a, p, k
 // host driver
 // ---------------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-static int po_seg(uint32_t flags) { return (flags & PICO_F_TINY_TILES) ? 4 : 256; }
+static int po_seg(uint32_t flags) { return (flags & PICO_F_TINY_TILES) ? 4 : 32; }
 
 size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags) {
     size_t b = 0;
@@ -332,10 +301,11 @@ size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags) {
     return b;
 }
 
-template <bool CLAMP_SUB, bool STATS>
+template <int MODE, bool STATS>
 static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                             cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st,
                             const DevInfo &dev) {
+    constexpr bool CLAMP_SUB = MODE == 1;
     PoArgs a;
     char *p = (char *)ws;
     a.ctl = (Ctrl *)p; p += align256(sizeof(Ctrl));
@@ -345,7 +315,6 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     a.alive1 = (int *)p; p += align256(sizeof(int) * (size_t)n);
     a.Q = (long long *)p;
     a.seg = po_seg(flags);
-    size_t qcap = (size_t)(n + arcs / a.seg + 64);
     a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core;
 
     cudaError_t err;
@@ -353,7 +322,6 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     h.kminb[0] = INT_MAX;
     h.kminb[1] = INT_MAX;
     if ((err = cudaMemcpyAsync(a.ctl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
-    if ((err = cudaMemsetAsync(a.Q, 0xff, sizeof(long long) * qcap, s))) return err;
 
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     auto tstart = [&](int slot) {
@@ -377,12 +345,12 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     tstop();
     if ((err = cudaGetLastError())) return err;
 
-    long long launches = 1;
+    long long launches = 1, host_subrounds = 0;
     tstart(PICO_K_PEEL);
     if (flags & PICO_F_HOST_LOOP) {
         int blocks = sms * 4;
         int k = 0, kprev = 0;
-        unsigned long long lstart = 0;
+        unsigned long long tail = 0;
         for (int L = 0;; L++) {
             int par = L & 1;
             Ctrl hc;
@@ -391,25 +359,39 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
             if (L > 0) { po_close_kernel<<<1, 1, 0, s>>>(a, par ^ 1, kprev); launches++; }
             if (hc.nAlive[par] == 0) break;
             k = std::max(k + 1, hc.kminb[par]);
+            unsigned long long lstart = hc.q_tail, lo = lstart;
             po_scan_kernel<STATS><<<blocks, 512, 0, s>>>(a, k, par);
-            po_drain_kernel<CLAMP_SUB, STATS><<<blocks, 512, 0, s>>>(a, k, par);
-            launches += 2;
-            if (CLAMP_SUB) {
-                unsigned long long lend = 0;
-                if ((err = cudaMemcpyAsync(&lend, &a.ctl->q_tail, sizeof(lend), cudaMemcpyDeviceToHost, s)))
+            launches++;
+            for (int sub = 0;; sub++) {
+                if ((err = cudaMemcpyAsync(&tail, &a.ctl->q_tail, sizeof(tail), cudaMemcpyDeviceToHost, s)))
                     return err;
                 if ((err = cudaStreamSynchronize(s))) return err;
-                if (lend > lstart) { po_repair_kernel<<<blocks, 512, 0, s>>>(a, k, lstart, lend); launches++; }
-                lstart = lend;
+                if (tail == lo) {
+                    if (sub == 0) {  // empty level: still consume alive[par]
+                        unsigned long long z = 0;
+                        int imax = INT_MAX;
+                        cudaMemcpyAsync(&a.ctl->nAlive[par], &z, sizeof(z), cudaMemcpyHostToDevice, s);
+                        cudaMemcpyAsync(&a.ctl->kminb[par], &imax, sizeof(imax), cudaMemcpyHostToDevice, s);
+                    }
+                    break;
+                }
+                po_sub_kernel<MODE, STATS><<<blocks, 512, 0, s>>>(a, k, par, lo, tail, sub == 0);
+                launches++;
+                host_subrounds++;
+                lo = tail;
+            }
+            if (CLAMP_SUB && lo > lstart) {
+                po_repair_kernel<<<blocks, 512, 0, s>>>(a, k, lstart, lo);
+                launches++;
             }
             kprev = k;
         }
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, po_levels_kernel<CLAMP_SUB, STATS>, 512, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, po_levels_kernel<MODE, STATS>, 512, 0);
         int per = std::max(1, std::min(occ, 2));
         void *args[] = {&a};
-        err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<CLAMP_SUB, STATS>, sms * per, 512,
+        err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<MODE, STATS>, sms * per, 512,
                                           args, 0, s);
         if (err) return err;
         launches++;
@@ -426,10 +408,10 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     if ((err = cudaStreamSynchronize(s))) return err;
     if (st) {
         st->levels = (int64_t)hc.levels;
+        st->subrounds = (flags & PICO_F_HOST_LOOP) ? host_subrounds : (int64_t)hc.rounds;
+        st->kmax = hc.kmax;
         st->segments = (int64_t)hc.q_tail;
         st->kernel_count = launches;
-        st->subrounds = (int64_t)hc.scans;
-        st->kmax = hc.kmax;
         if (st->frontier_sizes)
             for (unsigned long long i = 0; i < hc.levels && (int64_t)i < st->frontier_sizes_cap && i < kFszCap; i++)
                 st->frontier_sizes[i] = (int64_t)lv[i];
@@ -455,11 +437,16 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
 
 cudaError_t po_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev) {
-    bool sub = flags & PICO_F_CLAMP_SUB, stats = flags & PICO_F_STATS;
-    if (sub && stats) return po_run_t<true, true>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
-    if (sub) return po_run_t<true, false>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
-    if (stats) return po_run_t<false, true>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
-    return po_run_t<false, false>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
+    bool stats = flags & PICO_F_STATS;
+    int mode = (flags & PICO_F_CLAMP_CAS) ? 2 : (flags & PICO_F_CLAMP_SUB) ? 1 : 0;
+#define PO_CASE(M)                                                                      \
+    if (mode == M) return stats ? po_run_t<M, true>(rp, ci, n, arcs, core, s, flags, ws, st, dev) \
+                                : po_run_t<M, false>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
+    PO_CASE(0)
+    PO_CASE(1)
+    PO_CASE(2)
+#undef PO_CASE
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace pico

@@ -27,7 +27,8 @@ def _variants(algo):
         base += [pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
                  pico.F_PULL_ALWAYS | pico.F_HOST_LOOP, pico.F_PUSH_ONLY | pico.F_HOST_LOOP]
     if algo == "peelone":
-        base += [pico.F_CLAMP_SUB, pico.F_CLAMP_SUB | pico.F_HOST_LOOP, pico.F_CLAMP_SUB | pico.F_TINY_TILES]
+        base += [pico.F_CLAMP_SUB, pico.F_CLAMP_SUB | pico.F_HOST_LOOP, pico.F_CLAMP_SUB | pico.F_TINY_TILES,
+                 pico.F_CLAMP_CAS, pico.F_CLAMP_CAS | pico.F_HOST_LOOP, pico.F_CLAMP_CAS | pico.F_TINY_TILES]
     return base
 
 
@@ -64,6 +65,10 @@ def _check(rp, ci, algo, flags, ref=None, jac=None):
         assert st.kmax == (int(nz.max()) if nz.size else 0)
         # vertices processed per level sum to the non-isolated count
         assert int(fs[:st.levels].sum()) == nz.size
+        # bulk-synchronous sub-rounds of the dynamic frontier equal the
+        # level-synchronous reference's (deterministic under BSP draining)
+        _, _, lv, sr = oracle.peel_levels(rp, ci)
+        assert st.levels == lv and st.subrounds == sr, (st.subrounds, sr)
     return st
 
 
