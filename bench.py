@@ -368,14 +368,21 @@ def main():
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-both", dest="both", action="store_false")
     ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded path even at one rank (torchrun --nproc-per-node 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rule)")
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        # not launched by torchrun: launch one process per GPU ourselves
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000)] + sys.argv
+        return subprocess.call(cmd)
+    if world > 1 or args.gpus > 1 or args.sharded:
         from bench_sharded import bench_sharded
         return bench_sharded(args)
     return bench_single(args)

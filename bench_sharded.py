@@ -1,0 +1,136 @@
+"""bench.py --gpus N (N > 1, launched by torchrun): sharded HistoCore
+(SURVEY 8(e)).  One process per GPU, NCCL over NVLink/NVSwitch for the
+exchange (torch.distributed), libpico kernels for every compute step.
+
+A step = one complete sharded coreness computation of the graph (shard
+creation with the per-rank CSC build, degree exchange, init, every round's
+pack / all-gatherv / apply, result).  Timed with CUDA events bracketed by a
+barrier + synchronize on both sides; the step time is the MAX over ranks;
+value = m / that time ("scaling": "strong": the graph is fixed as N grows).
+Every rank builds the same seeded graph and uses only its own rows.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import numpy as np
+
+
+def bench_sharded(args):
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import sharded
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ex = sharded.TorchDistExchange()
+    stream = torch.cuda.current_stream(dev)
+
+    cfg, rp, ci = bench.build_graph(args.config, dev)
+    n, m = rp.numel() - 1, ci.numel() // 2
+    bounds = sharded.partition(rp, world)
+    vb, ve = bounds[rank], bounds[rank + 1]
+    rp_l, ci_l = sharded.local_rows(rp, ci, vb, ve)
+
+    def step():
+        shard = sharded.DeviceShard(rp_l, ci_l, vb, n, args.flags)
+        try:
+            return sharded.run_shard(shard, ex, dev)
+        finally:
+            shard.close()
+
+    for _ in range(args.warmup):
+        run = step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = bench.ClockSampler(local) if rank == 0 else None
+    if clk:
+        clk.__enter__()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        run = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if clk:
+        clk.__exit__(None, None, None)
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    ms = ex.max_over_ranks(ms_rank, dev)
+
+    # parity: the assembled coreness against the single-GPU path (itself
+    # bit-exact vs the oracle in tests and in the N=1 bench) on rank 0
+    counts = ex.allgather_counts(run.core_local.numel(), dev)
+    core = ex.allgatherv(run.core_local, counts)
+    parity = "skipped"
+    if rank == 0:
+        ref = pico.coreness(rp, ci)
+        parity = "bit-exact vs single-GPU" if torch.equal(core, ref) else "MISMATCH"
+        if not args.no_oracle and n * 1 <= (8 << 20):
+            import oracle
+            import synth
+            r_np, c_np = synth.to_numpy(rp, ci)
+            if np.array_equal(oracle.bz(r_np, c_np), core.cpu().numpy()):
+                parity = "bit-exact vs oracle"
+            else:
+                parity = "MISMATCH vs oracle"
+
+    # e2e: local rows from pinned host memory -> device, sharded run, result
+    # back to pinned host memory, per step
+    rp_h = rp_l.cpu().pin_memory()
+    ci_h = ci_l.cpu().pin_memory()
+    out_h = torch.empty(max(rp_l.numel() - 1, 1), dtype=torch.int32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 5))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        rp_d = rp_h.to(dev, non_blocking=True)
+        ci_d = ci_h.to(dev, non_blocking=True)
+        shard = sharded.DeviceShard(rp_d, ci_d, vb, n, args.flags)
+        try:
+            r2 = sharded.run_shard(shard, ex, dev)
+        finally:
+            shard.close()
+        out_h[:r2.core_local.numel()].copy_(r2.core_local, non_blocking=True)
+        torch.cuda.synchronize()
+    dist.barrier()
+    e2e_t = ex.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
+
+    if rank == 0:
+        peak, src = bench.hbm_peak()
+        launches = 12 + 4 * run.rounds
+        out = {
+            "metric": bench.METRIC, "value": m / (ms * 1e-3), "unit": bench.UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": cfg.note, "config": args.config, "algo": "histocore-sharded", "n": n, "m": m,
+                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL)",
+                       "l2_flush": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
+                         "traffic": None, "peak_source": src + f" x {world} GPUs",
+                         "note": "per-kernel sharded timings not instrumented; see the N=1 line"},
+            "cpu_baseline": None,
+            "e2e": {"value": m / e2e_t, "unit": bench.UNIT, "ms_per_step": 1e3 * e2e_t,
+                    "h2d_bytes_per_step": int(8 * n + 4 * 2 * m), "d2h_bytes_per_step": int(4 * n)},
+            "gpu_launches": launches * args.steps * world,
+            "clocks": clk.summary() if clk else None,
+            "parity": parity,
+            "iterations": {"histocore_l2": run.rounds},
+            "exchange": {"triples_per_step": run.triples_exchanged, "bytes_per_rank_per_step": 12 * run.triples_exchanged,
+                         "partition": bounds},
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

@@ -125,22 +125,20 @@ def _setup_shard(lib):
         return
     vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint32
     P64 = ctypes.POINTER(ctypes.c_int64)
-    lib.pico_shard_create.argtypes = [vp, vp, i64, i64, i64, vp, u32, ctypes.POINTER(vp)]
+    lib.pico_shard_create.argtypes = [vp, vp, i64, i64, i64, u32, vp, ctypes.POINTER(vp)]
     lib.pico_shard_create.restype = i32
-    lib.pico_shard_destroy.argtypes = [vp]
-    lib.pico_shard_destroy.restype = i32
+    lib.pico_shard_degrees.argtypes = [vp, vp]
+    lib.pico_shard_degrees.restype = i32
     lib.pico_shard_init.argtypes = [vp, vp, P64]
     lib.pico_shard_init.restype = i32
-    lib.pico_shard_pack.argtypes = [vp, vp, vp, i64, P64]
+    lib.pico_shard_pack.argtypes = [vp, vp, i64, P64]
     lib.pico_shard_pack.restype = i32
-    lib.pico_shard_apply.argtypes = [vp, vp, i64, vp, P64]
+    lib.pico_shard_apply.argtypes = [vp, vp, i64, P64]
     lib.pico_shard_apply.restype = i32
-    lib.pico_shard_sum.argtypes = [vp, vp, P64]
-    lib.pico_shard_sum.restype = i32
-    lib.pico_shard_result.argtypes = [vp, vp, vp]
+    lib.pico_shard_result.argtypes = [vp, vp]
     lib.pico_shard_result.restype = i32
-    lib.pico_shard_build_csc.argtypes = [vp, vp]
-    lib.pico_shard_build_csc.restype = i32
+    lib.pico_shard_destroy.argtypes = [vp]
+    lib.pico_shard_destroy.restype = i32
 
 
 def check(rc: int):

@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "pico_shard.h"
 
 namespace pico {
 
@@ -350,6 +351,87 @@ int pico_coreness_host(const int64_t *rowptr_h, const int32_t *colidx_h, int64_t
     e = cudaStreamSynchronize(s);
     if (e && rc == PICO_OK) rc = cuda_fail(e, "synchronize");
     return rc;
+}
+
+// ---------------------------------------------------------------------------
+// sharded HistoCore (include/pico_shard.h)
+// ---------------------------------------------------------------------------
+struct pico_shard_s {
+    Shard *impl;
+};
+
+int pico_shard_create(const int64_t *rowptr_local, const int32_t *colidx_local, int64_t nloc, int64_t v_begin,
+                      int64_t n_global, uint32_t flags, pico_stream_t stream, pico_shard_t *out) {
+    g_last_error.clear();
+    if (!out) return fail(PICO_EINVAL, "NULL output handle");
+    *out = nullptr;
+    if (nloc < 0 || v_begin < 0 || n_global <= 0 || v_begin + nloc > n_global)
+        return fail(PICO_EINVAL, "bad shard range [%lld, %lld) of %lld", (long long)v_begin,
+                    (long long)(v_begin + nloc), (long long)n_global);
+    if (n_global >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n_global needs 64-bit vertex ids");
+    if (!rowptr_local) return fail(PICO_EINVAL, "NULL rowptr_local");
+    DevInfo dev;
+    cudaError_t e = dev_info(&dev);
+    if (e) return cuda_fail(e, "device query");
+    Shard *impl = nullptr;
+    e = shard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags,
+                     (cudaStream_t)stream, dev, &impl);
+    if (e) return cuda_fail(e, "shard create");
+    *out = new pico_shard_s{impl};
+    return PICO_OK;
+}
+
+int pico_shard_degrees(pico_shard_t h, int32_t *deg_local) {
+    g_last_error.clear();
+    if (!h) return fail(PICO_EINVAL, "NULL shard");
+    cudaError_t e = shard_degrees(h->impl, deg_local);
+    return e ? cuda_fail(e, "shard degrees") : PICO_OK;
+}
+
+int pico_shard_init(pico_shard_t h, const int32_t *deg_global, int64_t *changed_local) {
+    g_last_error.clear();
+    if (!h || !deg_global || !changed_local) return fail(PICO_EINVAL, "NULL argument");
+    long long c = 0;
+    cudaError_t e = shard_init(h->impl, deg_global, &c);
+    if (e) return cuda_fail(e, "shard init");
+    *changed_local = c;
+    return PICO_OK;
+}
+
+int pico_shard_pack(pico_shard_t h, int32_t *triples, int64_t cap, int64_t *count) {
+    g_last_error.clear();
+    if (!h || !count || (cap > 0 && !triples)) return fail(PICO_EINVAL, "NULL argument");
+    long long c = 0;
+    cudaError_t e = shard_pack(h->impl, triples, cap, &c);
+    if (e == cudaErrorInvalidValue) return fail(PICO_EINVAL, "triple buffer too small (cap %lld)", (long long)cap);
+    if (e) return cuda_fail(e, "shard pack");
+    *count = c;
+    return PICO_OK;
+}
+
+int pico_shard_apply(pico_shard_t h, const int32_t *triples, int64_t total, int64_t *changed_local) {
+    g_last_error.clear();
+    if (!h || !changed_local || total < 0 || (total > 0 && !triples)) return fail(PICO_EINVAL, "bad argument");
+    long long c = 0;
+    cudaError_t e = shard_apply(h->impl, triples, total, &c);
+    if (e) return cuda_fail(e, "shard apply");
+    *changed_local = c;
+    return PICO_OK;
+}
+
+int pico_shard_result(pico_shard_t h, int32_t *core_local) {
+    g_last_error.clear();
+    if (!h) return fail(PICO_EINVAL, "NULL shard");
+    cudaError_t e = shard_result(h->impl, core_local);
+    return e ? cuda_fail(e, "shard result") : PICO_OK;
+}
+
+int pico_shard_destroy(pico_shard_t h) {
+    g_last_error.clear();
+    if (!h) return PICO_OK;
+    cudaError_t e = shard_destroy(h->impl);
+    delete h;
+    return e ? cuda_fail(e, "shard destroy") : PICO_OK;
 }
 
 }  // extern "C"

@@ -41,6 +41,8 @@
 //   oldcore[v] = core_old, histo[v][k] = sum.
 #include <climits>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -52,6 +54,12 @@ namespace pico {
 #endif
 #ifndef PICO_L2_HINTS
 #define PICO_L2_HINTS 0
+#endif
+// vertex count from which dense rounds may run UpdateHisto in the pull direction
+constexpr long long kPullMinN = 16ll << 20;
+// arcs per UpdateHisto work item (segment of a changed row)
+#ifndef PICO_HC_SEG
+#define PICO_HC_SEG 64
 #endif
 #if PICO_SHADOW_BITS == 8
 typedef unsigned char shadow_t;
@@ -82,6 +90,8 @@ struct HcArgs {
     Ctrl *ctl;
     Tune tn;
     int allow_pull;
+    const shadow_t *nv16;  // neighbour-degree lookups of InitHisto (see init_val)
+    const int *nv32;
 };
 
 // ---------------------------------------------------------------------------
@@ -120,8 +130,23 @@ __device__ __forceinline__ void warp_append_segments(int v, int nseg, int2 *S,
     unsigned long long base = 0;
     if (lane_id() == 0) base = atomicAdd(nS, (unsigned long long)total);
     base = __shfl_sync(FULL, base, 0);
-    unsigned long long off = base + (unsigned long long)(incl - nseg);
-    for (int s = 0; s < nseg; s++) S[off + s] = make_int2(v, s);
+    // the warp writes the `total` entries jointly (a hub's thousands of
+    // segments do not serialise on its lane): entry j belongs to the lane with
+    // the largest exclusive offset <= j
+    const int excl = incl - nseg;
+    for (int j0 = 0; j0 < total; j0 += 32) {
+        int j = j0 + lane_id();
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            int cand = lo + step;
+            int ex = __shfl_sync(FULL, excl, cand & 31);
+            if (cand < 32 && ex <= j) lo = cand;
+        }
+        int vo = __shfl_sync(FULL, v, lo);
+        int eo = __shfl_sync(FULL, excl, lo);
+        if (j < total) S[base + j] = make_int2(vo, j - eo);
+    }
 }
 
 __device__ __forceinline__ void stat_add(unsigned long long *ctr, long long x) {
@@ -185,10 +210,12 @@ __global__ void hc_degree_kernel(HcArgs a) {
 }
 
 // neighbour degree for init, clamped to d (the histogram cap of P:498)
+// (nv16 / nv32: degree of every neighbour id -- the local shadow / oldcore on
+// one GPU, the all-gathered global degrees on a shard)
 __device__ __forceinline__ int init_val(const HcArgs &a, int u, int d, unsigned long long hot) {
-    int x = (int)ld_shadow(a.c8 + u, hot);
+    int x = (int)ld_shadow(a.nv16 + u, hot);
     if (x >= d) return d;
-    if (x == (int)SAT8) return min(__ldg(a.oldc + u), d);
+    if (x == (int)SAT8) return min(__ldg(a.nv32 + u), d);
     return x;
 }
 
@@ -822,7 +849,7 @@ Tune hc_tune(uint32_t flags) {
     if (flags & PICO_F_TINY_TILES) {
         t.a_max = 4; t.b_max = 12; t.c_bins = 16; t.seg = 4;
     } else {
-        t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = 256;
+        t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = PICO_HC_SEG;
     }
     t.pull_div = 8;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
     if (flags & PICO_F_PULL_ALWAYS) t.pull_div = 1 << 30;
@@ -914,7 +941,12 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.chg = (unsigned *)(p + L.chg);
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)n; a.arcs = arcs; a.core = core; a.tn = tn;
-    a.allow_pull = (flags & PICO_F_PUSH_ONLY) ? 0 : 1;
+    // Pull pays when push's remote histogram RMWs and shadow gathers miss L2,
+    // i.e. on graphs whose per-vertex arrays outgrow it (measured: C2 push is
+    // 1.15x faster, RMAT-26 mixed push/pull 1.14x faster than push only).
+    a.allow_pull = (flags & PICO_F_PUSH_ONLY) ? 0 : (flags & PICO_F_PULL_ALWAYS) ? 1 : (n >= kPullMinN);
+    a.nv16 = a.c8;
+    a.nv32 = a.oldc;
 
     Timer tm{s, (flags & PICO_F_TIMING) != 0, {}};
     cudaError_t err;
@@ -1060,6 +1092,358 @@ cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long ar
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev) {
     if (flags & PICO_F_STATS) return hc_run_t<true>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
     return hc_run_t<false>(rp, ci, n, arcs, core, s, flags, ws, st, dev);
+}
+
+// ===========================================================================
+// Sharded HistoCore: rank r owns the rows of a contiguous vertex
+// range [vb, vb+nloc) with their histograms and estimates; a local CSC lists,
+// for every global vertex v, the owned neighbours u of v (the transpose of the
+// local row block -- the graph is symmetric).  One round t:
+//   pack:  changed (v, oldcore, core) triples of the local C_t   (this file)
+//   exchange: allgatherv of the triples over all ranks            (caller:
+//             torch.distributed / NCCL, paper_2402_15253_b200/sharded.py)
+//   apply: UpdateHisto of every received triple over CSC_r[v] -> local F_{t+1},
+//          then SumHisto(F_{t+1}) -> local C_{t+1}                (this file)
+// All state of an owned u lives on its owner, so the rounds are exactly the
+// synchronous rounds of the single-GPU path: same C_t, same l2 for every P.
+// ===========================================================================
+struct Shard {
+    HcArgs a;
+    void *ws;
+    long long nloc, vb, ng, arcs;
+    uint32_t flags;
+    cudaStream_t s;
+    DevInfo dev;
+    shadow_t *deg16g;        // [ng]   saturated global degrees (init)
+    long long *csc_off;      // [ng+1]
+    long long *csc_cur;      // [ng]
+    int *csc_idx;            // [arcs] owned neighbour (local id)
+    int2 *TS;                // (triple, segment) work items
+    long long tscap;
+    unsigned long long *cnt; // [4] device counters
+    void *cubtmp;
+    size_t cubbytes;
+    int t;
+};
+
+__global__ void sh_deg16_kernel(const int *deg, long long ng, shadow_t *d16) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < ng; v += nt)
+        d16[v] = (shadow_t)min(deg[v], (int)SAT8);
+}
+
+// CSC counts per global vertex (into csc_off[v+1]) and scatter
+__global__ void sh_csc_count_kernel(const int *ci, long long arcs, unsigned long long *cnt_v) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < arcs; e += nt)
+        atomicAdd(cnt_v + ci[e], 1ull);
+}
+
+__global__ void sh_csc_fill_kernel(const long long *rp, const int *ci, long long nloc, long long *cur,
+                                   int *idx) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = gw; u < nloc; u += nw)
+        for (long long e = rp[u] + lane_id(); e < rp[u + 1]; e += 32) {
+            unsigned long long pos = atomicAdd((unsigned long long *)(cur + ci[e]), 1ull);
+            idx[pos] = (int)u;
+        }
+}
+
+// C_t of this rank = segment-0 entries of S (init and SumHisto append one
+// (v, 0) per changed v) -> triples (v + vb, oldcore, core)
+__global__ void sh_pack_kernel(HcArgs a, long long ns, long long vb, int *out, unsigned long long *count) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    long long iters = (ns + nt - 1) / nt;
+    for (long long it = 0; it < iters; it++) {
+        long long i = it * nt + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        bool take = false;
+        int v = 0;
+        if (i < ns) {
+            int2 sg = a.S[i];
+            take = sg.y == 0;
+            v = sg.x;
+        }
+        unsigned m = __ballot_sync(FULL, take);
+        if (!m) continue;
+        unsigned long long base = 0;
+        int leader = __ffs(m) - 1;
+        if (lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (take) {
+            unsigned long long o = 3 * (base + __popc(m & ((1u << lane_id()) - 1)));
+            out[o] = (int)(v + vb);
+            out[o + 1] = a.oldc[v];
+            out[o + 2] = a.core[v];
+        }
+    }
+}
+
+// (triple, segment) items for the CSC lists of the received triples
+__global__ void sh_segments_kernel(const int *tr, long long total, const long long *csc_off, int seg, int2 *TS,
+                                   unsigned long long *nTS) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    long long iters = (total + nt - 1) / nt;
+    for (long long it = 0; it < iters; it++) {
+        long long i = it * nt + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        int ns = 0;
+        if (i < total) {
+            int v = tr[3 * i];
+            ns = nseg_of(csc_off[v + 1] - csc_off[v], seg);
+        }
+        warp_append_segments((int)i, ns, TS, nTS);
+    }
+}
+
+// UpdateHisto of the received triples over the local CSC (push direction)
+__global__ void __launch_bounds__(512, 2) sh_update_kernel(HcArgs a, const int *tr, const int2 *TS, long long nts,
+                                                           const long long *csc_off, const int *csc_idx,
+                                                           unsigned long long *nF) {
+    constexpr int U = 4;
+    const int lane = lane_id();
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long hot = pol_last();
+    for (long long base = gwarp * 32; base < nts; base += nwarps * 32) {
+        long long i = base + lane;
+        long long b = 0;
+        int len = 0, cv = 0, ov = 0;
+        if (i < nts) {
+            int2 sg = TS[i];
+            int v = tr[3 * sg.x];
+            ov = tr[3 * sg.x + 1];
+            cv = tr[3 * sg.x + 2];
+            long long r0 = csc_off[v], r1 = csc_off[v + 1];
+            b = r0 + (long long)sg.y * a.tn.seg;
+            len = (int)min((long long)a.tn.seg, r1 - b);
+        }
+        int incl = warp_incl_scan(len);
+        int excl = incl - len;
+        int total = __shfl_sync(FULL, incl, 31);
+        for (int j0 = 0; j0 < total; j0 += 32 * U) {
+            int u[U], cvo[U], ovo[U], cu[U];
+            bool ok[U], push[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                int j = j0 + q * 32 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    int cand = lo + step;
+                    int ex = __shfl_sync(FULL, excl, cand & 31);
+                    if (cand < 32 && ex <= j) lo = cand;
+                }
+                long long eb = __shfl_sync(FULL, b, lo);
+                int ex = __shfl_sync(FULL, excl, lo);
+                cvo[q] = __shfl_sync(FULL, cv, lo);
+                ovo[q] = __shfl_sync(FULL, ov, lo);
+                ok[q] = j < total;
+                u[q] = ok[q] ? csc_idx[eb + (j - ex)] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                cu[q] = ok[q] ? core_of(a, u[q], hot) : 0;
+                ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
+                push[q] = false;
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++)
+                if (ok[q]) push[q] = bin_move(a.histo, __ldg(a.rp + u[q]) - 1, cu[q], cvo[q], ovo[q]);
+            append_pushes<U>(push, u, a.F, nF);
+        }
+    }
+}
+
+size_t shard_workspace_bytes(long long nloc, long long ng, long long arcs, uint32_t flags, long long *tscap,
+                             size_t *cubbytes) {
+    Tune tn = hc_tune(flags);
+    size_t b = align256(hc_layout(nloc, arcs, flags).total);
+    b += align256(sizeof(shadow_t) * (size_t)ng);
+    b += align256(sizeof(long long) * (size_t)(ng + 1)) * 2;
+    b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
+    *tscap = ng + arcs / tn.seg + 64;
+    b += align256(sizeof(int2) * (size_t)*tscap);
+    b += align256(sizeof(unsigned long long) * 4);
+    b += align256(sizeof(int) * (size_t)std::max(nloc, 1ll));  // local core
+    size_t cb = 0;
+    cub::DeviceScan::ExclusiveSum((void *)nullptr, cb, (const long long *)nullptr, (long long *)nullptr, (int)(ng + 1));
+    *cubbytes = cb;
+    b += align256(cb);
+    return b;
+}
+
+cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, long long vb, long long ng,
+                         uint32_t flags, cudaStream_t s, const DevInfo &dev, Shard **out) {
+    Shard *h = new Shard();
+    h->nloc = nloc; h->vb = vb; h->ng = ng; h->flags = flags; h->s = s; h->dev = dev; h->t = 1;
+    cudaError_t e = cudaMemcpyAsync(&h->arcs, rp + nloc, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) { delete h; return e; }
+    size_t bytes = shard_workspace_bytes(nloc, ng, h->arcs, flags, &h->tscap, &h->cubbytes);
+    if ((e = cudaMallocAsync(&h->ws, bytes, s))) { delete h; return e; }
+    HcLayout L = hc_layout(nloc, h->arcs, flags);
+    char *p = (char *)h->ws;
+    HcArgs &a = h->a;
+    a.ctl = (Ctrl *)(p + L.ctl);
+    a.fsz = (unsigned long long *)(p + L.fsz);
+    a.rarcs = (unsigned long long *)(p + L.rarcs);
+    a.fsz_cap = kFszCap;
+    a.histo = (int *)(p + L.histo);
+    a.c8 = (shadow_t *)(p + L.c8);
+    a.oldc = (int *)(p + L.oldc);
+    a.F = (int *)(p + L.F);
+    a.BC = (int *)(p + L.BC);
+    a.S = (int2 *)(p + L.S);
+    a.H = (int2 *)(p + L.H);
+    a.chg = (unsigned *)(p + L.chg);
+    a.nwords = L.nwords;
+    a.rp = rp; a.ci = ci; a.n = (int)nloc; a.arcs = h->arcs; a.tn = hc_tune(flags);
+    a.allow_pull = 0;
+    p += align256(L.total);
+    h->deg16g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
+    h->csc_off = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
+    h->csc_cur = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
+    h->csc_idx = (int *)p; p += align256(sizeof(int) * (size_t)std::max(h->arcs, 1ll));
+    h->TS = (int2 *)p; p += align256(sizeof(int2) * (size_t)h->tscap);
+    h->cnt = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * 4);
+    a.core = (int *)p; p += align256(sizeof(int) * (size_t)std::max(nloc, 1ll));
+    h->cubtmp = p;
+    Ctrl hc{};
+    hc.mincv[0] = hc.mincv[1] = INT_MAX;
+    if (!e) e = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)L.nwords, s);
+    // H0 on the owned rows: core = oldcore = deg, shadow, degree classes
+    int blocks = (int)std::min<long long>((nloc + 255) / 256, (long long)dev.sms * 16);
+    if (!e && nloc > 0) {
+        hc_degree_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+        e = cudaGetLastError();
+    }
+    if (e) {
+        cudaFreeAsync(h->ws, s);
+        delete h;
+        return e;
+    }
+    *out = h;
+    return cudaSuccess;
+}
+
+cudaError_t shard_degrees(Shard *h, int *deg_out) {
+    if (h->nloc == 0) return cudaSuccess;
+    return cudaMemcpyAsync(deg_out, h->a.core, sizeof(int) * (size_t)h->nloc, cudaMemcpyDeviceToDevice, h->s);
+}
+
+// InitHisto + round-1 SumHisto of the owned rows (neighbour degrees from the
+// all-gathered deg_global) and the local CSC
+cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
+    cudaStream_t s = h->s;
+    HcArgs &a = h->a;
+    const int sms = h->dev.sms;
+    auto grid = [&](long long work) {
+        return std::max(1, (int)std::min<long long>((work + 255) / 256, (long long)sms * 16));
+    };
+    cudaError_t e;
+    sh_deg16_kernel<<<grid(h->ng), 256, 0, s>>>(deg_global, h->ng, h->deg16g);
+    a.nv16 = h->deg16g;
+    a.nv32 = deg_global;
+    // CSC: counts -> exclusive scan -> scatter
+    if ((e = cudaMemsetAsync(h->csc_cur, 0, sizeof(long long) * (size_t)(h->ng + 1), s))) return e;
+    if (h->arcs)
+        sh_csc_count_kernel<<<grid(h->arcs), 256, 0, s>>>(a.ci, h->arcs, (unsigned long long *)h->csc_cur);
+    size_t cb = h->cubbytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(h->cubtmp, cb, h->csc_cur, h->csc_off, (int)(h->ng + 1), s))) return e;
+    if ((e = cudaMemcpyAsync(h->csc_cur, h->csc_off, sizeof(long long) * (size_t)h->ng, cudaMemcpyDeviceToDevice, s)))
+        return e;
+    if (h->nloc) sh_csc_fill_kernel<<<sms * 8, 256, 0, s>>>(a.rp, a.ci, h->nloc, h->csc_cur, h->csc_idx);
+    // InitHisto fused with round-1 SumHisto (the single-GPU init kernels)
+    if (h->nloc) {
+        Tune tn = a.tn;
+        hc_init_small_kernel<false><<<grid(h->nloc), 256, 0, s>>>(a);
+        size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
+        cudaFuncSetAttribute(hc_init_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+        hc_init_warp_kernel<false><<<sms * 4, 256, smB, s>>>(a);
+        size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
+        cudaFuncSetAttribute(hc_init_cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC);
+        hc_init_cta_kernel<false><<<sms, 512, smC, s>>>(a);
+        hc_init_fallback_kernel<false><<<sms, 512, 0, s>>>(a);
+        hc_shadow_kernel<<<grid(h->nloc), 256, 0, s>>>(a);
+    }
+    a.nv16 = a.c8;
+    a.nv32 = a.oldc;
+    unsigned long long c1 = 0;
+    if ((e = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if ((e = cudaGetLastError())) return e;
+    *changed = (long long)c1;
+    h->t = 1;
+    return cudaSuccess;
+}
+
+cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count) {
+    cudaStream_t s = h->s;
+    cudaError_t e;
+    unsigned long long ns = 0;
+    if ((e = cudaMemcpyAsync(&ns, &h->a.ctl->nS[h->t & 1], sizeof(ns), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaMemsetAsync(h->cnt, 0, sizeof(unsigned long long), s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (ns) {
+        int blocks = (int)std::min<long long>(((long long)ns + 255) / 256, (long long)h->dev.sms * 16);
+        sh_pack_kernel<<<std::max(blocks, 1), 256, 0, s>>>(h->a, (long long)ns, h->vb, triples, h->cnt);
+    }
+    unsigned long long c = 0;
+    if ((e = cudaMemcpyAsync(&c, h->cnt, sizeof(c), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if ((long long)c > cap) return cudaErrorInvalidValue;
+    *count = (long long)c;
+    return cudaGetLastError();
+}
+
+// UpdateHisto(C_t of all ranks) over the local CSC, then SumHisto(F_{t+1})
+cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed) {
+    cudaStream_t s = h->s;
+    HcArgs &a = h->a;
+    const int sms = h->dev.sms;
+    const int t = h->t;
+    cudaError_t e;
+    unsigned long long *nTS = h->cnt + 1;
+    if ((e = cudaMemsetAsync(nTS, 0, sizeof(unsigned long long), s))) return e;
+    if ((e = cudaMemsetAsync(&a.ctl->nF[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
+    if ((e = cudaMemsetAsync(&a.ctl->nS[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
+    unsigned long long nts = 0;
+    if (total > 0) {
+        int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+        sh_segments_kernel<<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->csc_off, a.tn.seg, h->TS, nTS);
+        if ((e = cudaMemcpyAsync(&nts, nTS, sizeof(nts), cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        if ((long long)nts > h->tscap) return cudaErrorInvalidValue;
+        if (nts)
+            sh_update_kernel<<<sms * 2, 512, 0, s>>>(a, triples, h->TS, (long long)nts, h->csc_off, h->csc_idx,
+                                                     &a.ctl->nF[(t + 1) & 1]);
+    }
+    unsigned long long nf = 0;
+    if ((e = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (nf) {
+        int sb = (int)std::min<long long>(((long long)nf + 511) / 512, (long long)sms * 4);
+        hc_sum_kernel<false><<<std::max(sb, 1), 512, 0, s>>>(a, t + 1);
+    }
+    if ((e = cudaStreamSynchronize(s))) return e;
+    h->t = t + 1;
+    *changed = (long long)nf;
+    return cudaGetLastError();
+}
+
+cudaError_t shard_result(Shard *h, int *core_out) {
+    if (h->nloc == 0) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(core_out, h->a.core, sizeof(int) * (size_t)h->nloc, cudaMemcpyDeviceToDevice, h->s);
+    if (!e) e = cudaStreamSynchronize(h->s);
+    return e;
+}
+
+cudaError_t shard_destroy(Shard *h) {
+    cudaError_t e = cudaFreeAsync(h->ws, h->s);
+    if (!e) e = cudaStreamSynchronize(h->s);
+    delete h;
+    return e;
 }
 
 }  // namespace pico

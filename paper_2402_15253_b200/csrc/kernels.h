@@ -43,6 +43,17 @@ cudaError_t relabel_build(const long long *rp, const int *ci, long long n, long 
                           void *ws, const DevInfo &dev, bool force, Relabel *out);
 cudaError_t relabel_back(const Relabel &r, long long n, int *core_out, cudaStream_t s, const DevInfo &dev);
 
+// sharded HistoCore (histocore.cu)
+struct Shard;
+cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, long long vb, long long ng,
+                         uint32_t flags, cudaStream_t s, const DevInfo &dev, Shard **out);
+cudaError_t shard_degrees(Shard *h, int *deg_out);
+cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed);
+cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count);
+cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed);
+cudaError_t shard_result(Shard *h, int *core_out);
+cudaError_t shard_destroy(Shard *h);
+
 size_t validate_workspace_bytes();
 cudaError_t validate_run(const long long *rp, const int *ci, long long n, long long arcs,
                          cudaStream_t s, void *ws, int *bad);

@@ -1,0 +1,237 @@
+"""Sharded (multi-GPU) HistoCore driver -- SURVEY 8(e); PAPER.md P:894 lists
+multi-GPU as future work.
+
+The compute of every step runs in libpico's kernels (include/pico_shard.h).
+This module is the plumbing between the steps:
+  * the arc-balanced 1-D vertex partition;
+  * the exchange: all-gather of the per-rank counts (which is also the global
+    convergence test: a round with a global count of 0 ends the run) and an
+    all-gather(v) of the changed (v, oldcore, core) triples;
+  * the round loop.
+
+Exchanges:
+  * TorchDistExchange -- torch.distributed (NCCL over NVLink/NVSwitch on B200,
+    gloo on CPU for the host-logic tests), one process per GPU;
+  * loopback -- P logical shards in one process on one GPU, the all-gather is
+    a device concatenation (coreness_loopback); this is how the sharded kernels
+    are parity-tested on a single GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import check, load
+
+
+# ---------------------------------------------------------------------------
+# partition (host logic)
+# ---------------------------------------------------------------------------
+def partition(rowptr, nparts: int) -> list[int]:
+    """Vertex boundaries [b_0 = 0, b_1, ..., b_P = n] of contiguous ranges
+    with ~2m/P arcs each: b_r = first v with rowptr[v] >= r * 2m / P."""
+    rp = np.asarray(rowptr if not hasattr(rowptr, "cpu") else rowptr.cpu().numpy(), dtype=np.int64)
+    n = rp.size - 1
+    arcs = int(rp[-1])
+    bounds = [0]
+    for r in range(1, nparts):
+        target = (arcs * r) // nparts
+        b = int(np.searchsorted(rp, target, side="left"))
+        bounds.append(min(max(b, bounds[-1]), n))
+    bounds.append(n)
+    return bounds
+
+
+def local_rows(rowptr, colidx, vb: int, ve: int):
+    """Rows [vb, ve) as (rowptr_local with rowptr_local[0] = 0, colidx_local)."""
+    a, b = int(rowptr[vb]), int(rowptr[ve])
+    rp = rowptr[vb:ve + 1] - a
+    return rp.contiguous(), colidx[a:b].contiguous()
+
+
+# ---------------------------------------------------------------------------
+# exchanges
+# ---------------------------------------------------------------------------
+class TorchDistExchange:
+    """allgather / allgatherv over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allgather_counts(self, count: int, device) -> list[int]:
+        import torch
+        t = torch.tensor([count], dtype=torch.int64, device=device)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+    def allgatherv(self, local, counts: list[int]):
+        """Concatenation in rank order of every rank's `local[:counts[rank]]`
+        (1-D tensors); all-gather of max-padded buffers."""
+        import torch
+        mx = max(counts)
+        if mx == 0:
+            return local[:0]
+        buf = torch.zeros(mx, dtype=local.dtype, device=local.device)
+        buf[:counts[self.rank]] = local[:counts[self.rank]]
+        out = [torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(out, buf, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(out, counts)])
+
+    def max_over_ranks(self, x: float, device) -> float:
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# one rank's shard (ctypes wrapper of pico_shard_*)
+# ---------------------------------------------------------------------------
+class DeviceShard:
+    """The rank's state in libpico (owned rows [vb, vb + nloc))."""
+
+    def __init__(self, rowptr_local, colidx_local, vb: int, n_global: int, flags: int = 0, stream=None):
+        import torch
+        self.lib = load()
+        self.dev = rowptr_local.device
+        self.rp, self.ci = rowptr_local, colidx_local  # kept alive for the handle
+        self.nloc = rowptr_local.numel() - 1
+        self.vb, self.n_global = vb, n_global
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        h = ctypes.c_void_p()
+        check(self.lib.pico_shard_create(self.rp.data_ptr(), self.ci.data_ptr() if self.ci.numel() else None,
+                                         self.nloc, vb, n_global, flags, ctypes.c_void_p(self.stream.cuda_stream),
+                                         ctypes.byref(h)))
+        self.h = h
+        self.trip = torch.empty(3 * max(self.nloc, 1), dtype=torch.int32, device=self.dev)
+
+    def degrees(self):
+        import torch
+        d = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=self.dev)
+        check(self.lib.pico_shard_degrees(self.h, d.data_ptr()))
+        return d[:self.nloc]
+
+    def init(self, deg_global) -> int:
+        c = ctypes.c_int64()
+        check(self.lib.pico_shard_init(self.h, deg_global.data_ptr(), ctypes.byref(c)))
+        return c.value
+
+    def pack(self):
+        c = ctypes.c_int64()
+        check(self.lib.pico_shard_pack(self.h, self.trip.data_ptr(), self.trip.numel() // 3, ctypes.byref(c)))
+        return self.trip, c.value
+
+    def apply(self, triples, total: int) -> int:
+        c = ctypes.c_int64()
+        check(self.lib.pico_shard_apply(self.h, triples.data_ptr() if total else None, total, ctypes.byref(c)))
+        return c.value
+
+    def result(self):
+        import torch
+        out = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=self.dev)
+        check(self.lib.pico_shard_result(self.h, out.data_ptr()))
+        return out[:self.nloc]
+
+    def close(self):
+        if self.h:
+            check(self.lib.pico_shard_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ShardRun:
+    core_local: object
+    rounds: int = 0
+    frontier_sizes: list = field(default_factory=list)
+    triples_exchanged: int = 0
+
+
+def run_shard(shard, exchange, device) -> ShardRun:
+    """The sharded HistoCore round loop for one rank.
+
+    shard: DeviceShard (or any object with degrees/init/pack/apply/result);
+    exchange: TorchDistExchange (or any object with allgather_counts /
+    allgatherv).  Returns this rank's coreness and the global |C_t| sequence
+    (|C_t| = |F_t|, Theorem 2), whose length is l2."""
+    deg_local = shard.degrees()
+    counts = exchange.allgather_counts(int(deg_local.numel()), device)
+    deg_global = exchange.allgatherv(deg_local, counts)
+    shard.init(deg_global)
+    run = ShardRun(core_local=None)
+    while True:
+        trip, cnt = shard.pack()
+        counts = exchange.allgather_counts(cnt, device)
+        total = sum(counts)
+        if total == 0:  # global convergence: no estimate changed anywhere
+            break
+        run.rounds += 1
+        run.frontier_sizes.append(total)
+        run.triples_exchanged += total
+        allt = exchange.allgatherv(trip, [3 * c for c in counts])
+        shard.apply(allt, total)
+    run.core_local = shard.result()
+    return run
+
+
+def coreness_sharded(rowptr, colidx, group=None, flags: int = 0) -> ShardRun:
+    """Sharded HistoCore of the full graph (rowptr/colidx on this rank's GPU;
+    only this rank's rows are used): one process per GPU, torch.distributed
+    group.  Returns this rank's ShardRun (core_local of its vertex range)."""
+    ex = TorchDistExchange(group)
+    bounds = partition(rowptr, ex.world)
+    vb, ve = bounds[ex.rank], bounds[ex.rank + 1]
+    rp_l, ci_l = local_rows(rowptr, colidx, vb, ve)
+    shard = DeviceShard(rp_l, ci_l, vb, rowptr.numel() - 1, flags)
+    try:
+        run = run_shard(shard, ex, rowptr.device)
+    finally:
+        shard.close()
+    run.v_begin, run.v_end = vb, ve
+    return run
+
+
+# ---------------------------------------------------------------------------
+# loopback: P logical shards on one GPU (parity of the sharded kernels)
+# ---------------------------------------------------------------------------
+def coreness_loopback(rowptr, colidx, nparts: int, flags: int = 0):
+    """P shards in one process; the exchange is a device concatenation.
+    Returns (coreness of all vertices, rounds l2, [|C_t|])."""
+    import torch
+    n = rowptr.numel() - 1
+    bounds = partition(rowptr, nparts)
+    shards = []
+    try:
+        for r in range(nparts):
+            rp_l, ci_l = local_rows(rowptr, colidx, bounds[r], bounds[r + 1])
+            shards.append(DeviceShard(rp_l, ci_l, bounds[r], n, flags))
+        deg = torch.cat([s.degrees() for s in shards])
+        for s in shards:
+            s.init(deg)
+        sizes = []
+        while True:
+            packs = [s.pack() for s in shards]
+            total = sum(c for _, c in packs)
+            if total == 0:
+                break
+            sizes.append(total)
+            allt = torch.cat([t[:3 * c] for t, c in packs])
+            for s in shards:
+                s.apply(allt, total)
+        core = torch.cat([s.result() for s in shards])
+    finally:
+        for s in shards:
+            s.close()
+    return core, len(sizes), sizes

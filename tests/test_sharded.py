@@ -1,0 +1,203 @@
+"""T7: sharded HistoCore.
+
+CPU: the partition, and the exchange / round protocol of
+paper_2402_15253_b200.sharded.run_shard over a real torch.distributed gloo
+group of world size 2.  The shard compute there is a test-only mock: the plain
+synchronous Index2core iteration (Alg 2) on the rank's owned
+vertices, whose changed sets are exactly HistoCore's C_t.
+
+GPU: the real shard kernels (include/pico_shard.h) in loopback mode -- P
+logical shards on one GPU, exchange = device concatenation -- against the
+oracle (coreness bit-exact, l2 and every |C_t| equal to the Jacobi sweeps)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2402_15253_b200 import sharded
+
+
+# ---------------------------------------------------------------- partition
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_partition_arc_balanced(parts):
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R14"].build())
+    b = sharded.partition(rp, parts)
+    assert b[0] == 0 and b[-1] == rp.size - 1 and len(b) == parts + 1
+    assert all(x <= y for x, y in zip(b, b[1:]))
+    arcs = int(rp[-1])
+    dmax = int(np.diff(rp).max())
+    for r in range(parts):
+        got = int(rp[b[r + 1]] - rp[b[r]])
+        assert abs(got - arcs / parts) <= dmax + 1  # balanced up to one row
+
+
+def test_partition_degenerate():
+    rp = np.array([0, 0, 0, 2, 2, 4], dtype=np.int64)  # isolated + small rows
+    b = sharded.partition(rp, 4)
+    assert b[0] == 0 and b[-1] == 5 and sorted(b) == b
+
+
+def test_local_rows_slices():
+    rp, ci = synth.CONFIGS["R12"].build()
+    b = sharded.partition(rp, 3)
+    total = 0
+    for r in range(3):
+        rl, cl = sharded.local_rows(rp, ci, b[r], b[r + 1])
+        assert int(rl[0]) == 0 and int(rl[-1]) == cl.numel()
+        total += cl.numel()
+    assert total == ci.numel()
+
+
+# ------------------------------------------------- mock shard (test only)
+class JacobiShard:
+    """Owned vertices [vb, ve): synchronous Index2core on a replica of every
+    neighbour's estimate, updated only from exchanged triples."""
+
+    def __init__(self, rp_l, ci_l, vb, n_global):
+        self.rp, self.ci = rp_l, ci_l
+        self.vb, self.nloc = vb, rp_l.size - 1
+        self.pending = []
+
+    def degrees(self):
+        return torch.from_numpy(np.diff(self.rp).astype(np.int32))
+
+    def init(self, deg_global):
+        self.rep = deg_global.numpy().astype(np.int64).copy()
+        self.val = np.diff(self.rp).astype(np.int64)
+        self._sweep()
+
+    def _sweep(self):
+        new = np.array([oracle.hindex(self.rep[self.ci[self.rp[v]:self.rp[v + 1]]])
+                        for v in range(self.nloc)], dtype=np.int64)
+        ch = np.flatnonzero(new != self.val)
+        self.pending = [(self.vb + v, int(self.val[v]), int(new[v])) for v in ch]
+        self.val = new
+
+    def pack(self):
+        flat = np.array(self.pending, dtype=np.int32).reshape(-1)
+        return torch.from_numpy(flat if flat.size else np.zeros(3, np.int32)), len(self.pending)
+
+    def apply(self, triples, total):
+        t = triples.numpy().reshape(-1, 3)
+        for v, old, new in t:
+            assert self.rep[v] == old
+            self.rep[v] = new
+        self._sweep()
+        return len(self.pending)
+
+    def result(self):
+        return torch.from_numpy(self.val.astype(np.int32))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, cfg, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rp, ci = synth.CONFIGS[cfg].build() if cfg in synth.CONFIGS else synth.g1()
+        rpn, cin = synth.to_numpy(rp, ci)
+        ex = sharded.TorchDistExchange()
+        b = sharded.partition(rpn, world)
+        rl, cl = sharded.local_rows(rp, ci, b[rank], b[rank + 1])
+        shard = JacobiShard(rl.numpy(), cl.numpy(), b[rank], rpn.size - 1)
+        run = sharded.run_shard(shard, ex, torch.device("cpu"))
+        counts = ex.allgather_counts(run.core_local.numel(), torch.device("cpu"))
+        core = ex.allgatherv(run.core_local, counts)
+        if rank == 0:
+            out.put((core.numpy().tolist(), run.rounds, run.frontier_sizes))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", ["G1", "R12"])
+def test_gloo_world2_protocol(cfg):
+    """world_size 2 over gloo: the sharded round protocol (count all-gather =
+    convergence test, triple all-gatherv, rank-ordered degree exchange) yields
+    the oracle coreness, l2 and |C_t| sequence."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    core, rounds, sizes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rp, ci = synth.to_numpy(*(synth.CONFIGS[cfg].build() if cfg in synth.CONFIGS else synth.g1()))
+    assert core == oracle.bz(rp, ci).tolist()
+    _, l2, fs = oracle.jacobi_rounds(rp, ci)
+    assert rounds == l2 and sizes == fs
+
+
+def test_shard_capi_argument_errors():
+    import ctypes
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import build
+    build.build()
+    lib = pico.load()
+    h = ctypes.c_void_p()
+    rp = np.zeros(3, dtype=np.int64)
+    # range beyond n_global / negative / NULL out
+    assert lib.pico_shard_create(rp.ctypes.data, None, 2, 5, 4, 0, None, ctypes.byref(h)) == 1
+    assert lib.pico_shard_create(rp.ctypes.data, None, -1, 0, 4, 0, None, ctypes.byref(h)) == 1
+    assert lib.pico_shard_create(rp.ctypes.data, None, 2, 0, 4, 0, None, None) == 1
+    assert lib.pico_shard_destroy(None) == 0
+
+
+# ---------------------------------------------------------------- GPU
+def _graphs():
+    from conftest import csr_np, parse_g1
+    g = parse_g1()
+    edges = [tuple(int(x) for x in p.split("-")) for p in g["edges"].split()]
+    out = [("G1", csr_np(6, edges)),
+           ("K20", csr_np(20, [(i, j) for i in range(20) for j in range(i + 1, 20)])),
+           ("star", csr_np(101, [(0, i) for i in range(1, 101)]))]
+    for i, (n, p) in enumerate([(150, 0.05), (200, 0.2)]):
+        out.append((f"er{i}", synth.to_numpy(*synth.erdos_renyi(n, p, seed=3000 + i))))
+    out.append(("cl", synth.to_numpy(*synth.chung_lu(3000, 10.0, 2.2, seed=3100))))
+    out.append(("R12", synth.to_numpy(*synth.CONFIGS["R12"].build())))
+    out.append(("R14", synth.to_numpy(*synth.CONFIGS["R14"].build())))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_loopback_parity(parts):
+    import paper_2402_15253_b200 as pico
+    dev = torch.device("cuda:0")
+    for name, (rp, ci) in _graphs():
+        ref = oracle.bz(rp, ci)
+        _, l2, fs = oracle.jacobi_rounds(rp, ci)
+        for fl in (0, pico.F_TINY_TILES):
+            core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
+                                                            torch.from_numpy(ci).to(dev), parts, fl)
+            got = core.cpu().numpy()
+            assert np.array_equal(got, ref), (name, parts, fl, np.flatnonzero(got != ref)[:5])
+            assert rounds == l2 and sizes == fs, (name, parts, fl)
+
+
+@pytest.mark.gpu
+def test_loopback_c1():
+    rp, ci = synth.to_numpy(*synth.CONFIGS["C1"].build())
+    dev = torch.device("cuda:0")
+    ref = oracle.bz(rp, ci)
+    _, l2, fs = oracle.jacobi_rounds(rp, ci)
+    for parts in (2, 8):
+        core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
+                                                        torch.from_numpy(ci).to(dev), parts)
+        assert np.array_equal(core.cpu().numpy(), ref) and rounds == l2 and sizes == fs
