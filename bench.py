@@ -46,13 +46,18 @@ def log(*a):
 # bytes"; SURVEY 8(d) 4-byte access model, each logical access counted once)
 # ---------------------------------------------------------------------------
 def hc_bytes(n: int, m: int, st: dict, f1: int, relabelled: bool = False) -> dict:
+    """B_alg = 8(n+1) + 4*2m [colidx] + 4*2m [gather deg] + 4*W1
+    [init slots] + 12n [core/oldcore init, initial cnt] + sum_t (32|F_t| +
+    4 bins_t + 8 S_t + 16 G_t), split by kernel slot: degree = rowptr + the
+    two estimate arrays; init = colidx + degree gathers + W1 + core + the
+    round-1 frontier (32|F_1|); rounds = the per-round terms for t >= 2 with
+    S_t = arcs scanned (push: rows of C_t; pull: rows streamed) and G_t =
+    guarded arcs (two 4 B read + 4 B write RMWs)."""
     arcs = 2 * m
-    segs, s1 = st["segments"], st["segments_init"]
     degree = 8 * (n + 1) + 8 * n
-    init = 8 * (n + 1) + 8 * arcs + 4 * st["init_slots_written"] + 4 * n + 8 * s1
-    rounds = (32 * segs + 8 * st["arcs_scanned"] + 24 * st["guarded_arcs"] + 4 * st["pushes"]
-              + 36 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * (segs - s1)
-              + 10 * n * st.get("pull_rounds", 0))  # pull: rowptr + core16 of every row
+    init = 8 * arcs + 4 * st["init_slots_written"] + 4 * n + 32 * f1
+    rounds = (32 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * st["arcs_scanned"]
+              + 16 * st["guarded_arcs"])
     out = {"degree": degree, "init": init, "rounds": rounds}
     if relabelled:
         out["relabel"] = relabel_bytes(n, m)
@@ -68,8 +73,12 @@ def relabel_bytes(n: int, m: int) -> int:
 
 
 def po_bytes(n: int, m: int, st: dict, relabelled: bool = False) -> dict:
+    """B_alg = 16n + 4*2m [colidx] + 4*2m [guard reads] + 8*G
+    [clamped RMW] + 8*pushes + 4*sum_k |alive_k| + 4n; degree slot = rowptr +
+    core + alive list, peel slot = the rest (rowptr of each processed row)."""
     degree = 8 * (n + 1) + 8 * n
-    peel = 12 * st["alive_scanned"] + 32 * st["segments"] + 8 * st["arcs_scanned"] + 8 * st["guarded_arcs"]
+    peel = (16 * n + 8 * st["arcs_scanned"] + 8 * st["guarded_arcs"] + 8 * st["pushes"]
+            + 4 * st["alive_scanned"])
     out = {"degree": degree, "peel": peel}
     if relabelled:
         out["relabel"] = relabel_bytes(n, m)
@@ -128,6 +137,14 @@ class ClockSampler:
                 self.proc.kill()
                 out = ""
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if not self.lines:  # timed region shorter than the sampling period
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                pass
 
     def summary(self):
         if not getattr(self, "lines", None):
@@ -360,7 +377,7 @@ def bench_single(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--algo", default="histocore", choices=["histocore", "peelone"])

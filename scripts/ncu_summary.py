@@ -1,0 +1,109 @@
+#!/usr/bin/env python
+"""Summarise ncu captures of one bench step into profiles/.
+
+    python scripts/ncu_summary.py CONFIG ALGO REPORT.ncu-rep [--out profiles/ncu_traffic.json]
+                                  [--md profiles/r01/ncu_CONFIG_ALGO.md]
+
+Maps kernels to bench.py's kernel slots (degree / init / rounds / peel /
+relabel), sums dram__bytes_read.sum + dram__bytes_write.sum and
+gpu__time_duration.sum per slot (one step = one launch of every slot kernel),
+merges the per-slot DRAM bytes into the JSON that bench.py reports as
+roofline.traffic, and writes a human-readable table of the key metrics.
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+SLOTS = [
+    ("rounds", ("hc_rounds_kernel",)),
+    ("init", ("hc_init_small", "hc_init_warp", "hc_init_cta", "hc_init_fallback", "hc_shadow")),
+    ("degree", ("hc_degree_kernel", "po_init_kernel")),
+    ("peel", ("po_levels_kernel",)),
+    ("relabel", ("rl_bits", "rl_rows", "rl_arcs", "rl_back", "DeviceScan")),
+]
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+           "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_red.sum"]
+SCALE = {"gpu__time_duration.sum": {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0},
+         "dram__bytes_read.sum": {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12},
+         "dram__bytes_write.sum": {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}}
+
+
+def slot_of(name):
+    for slot, keys in SLOTS:
+        if any(k in name for k in keys):
+            return slot
+    return None
+
+
+def main():
+    cfg, algo, rep = sys.argv[1:4]
+    out = "profiles/ncu_traffic.json"
+    md = None
+    if "--out" in sys.argv:
+        out = sys.argv[sys.argv.index("--out") + 1]
+    if "--md" in sys.argv:
+        md = sys.argv[sys.argv.index("--md") + 1]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    agg, lines, seen = {}, [], set()
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        name = d.get("Kernel Name", "")
+        # one step = one launch of each distinct kernel (the bench's STATS run
+        # and timed runs use different template instances of the same kernel)
+        base = name.split("<")[0].split("(")[0].replace("void ", "").strip()
+        if base in seen:
+            continue
+        seen.add(base)
+        slot = slot_of(name)
+        vals = {}
+        for mtr in METRICS:
+            try:
+                v = float(d[mtr].replace(",", ""))
+            except Exception:
+                continue
+            if v != v:  # nan (metric not collected for this launch)
+                continue
+            vals[mtr] = v * SCALE.get(mtr, {}).get(u.get(mtr, ""), 1.0)
+        lines.append((name[:60], slot, vals))
+        if slot is None:
+            continue
+        a = agg.setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": []})
+        a["dram_bytes_per_step"] += vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0)
+        a["time_s"] += vals.get("gpu__time_duration.sum", 0)
+        a["kernels"].append(name[:60])
+    try:
+        with open(out) as f:
+            allj = json.load(f)
+    except Exception:
+        allj = {}
+    allj.setdefault(cfg, {})[algo] = {k: {"dram_bytes_per_step": v["dram_bytes_per_step"],
+                                          "ncu_time_s": v["time_s"], "kernels": v["kernels"],
+                                          "source": rep} for k, v in agg.items()}
+    with open(out, "w") as f:
+        json.dump(allj, f, indent=1, sort_keys=True)
+    if md:
+        with open(md, "w") as f:
+            f.write(f"# ncu --set full summary: {cfg} {algo} ({rep})\n\n")
+            f.write("ncu replays each kernel with cold caches and serialised launches: times are for shares, "
+                    "not absolutes.\n\n")
+            f.write("| kernel | slot | time ms | DRAM read GB | DRAM write GB | L2 hit % | warps active % | L2 thru % | regs |\n")
+            f.write("|---|---|---|---|---|---|---|---|---|\n")
+            for name, slot, v in lines:
+                f.write(f"| `{name}` | {slot} | {v.get('gpu__time_duration.sum', 0) * 1e3:.3f} | "
+                        f"{v.get('dram__bytes_read.sum', 0) / 1e9:.3f} | {v.get('dram__bytes_write.sum', 0) / 1e9:.3f} | "
+                        f"{v.get('lts__t_sector_hit_rate.pct', 0):.1f} | "
+                        f"{v.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
+                        f"{v.get('lts__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
+                        f"{v.get('launch__registers_per_thread', 0):.0f} |\n")
+    print(json.dumps(allj[cfg][algo], indent=1))
+
+
+if __name__ == "__main__":
+    main()
