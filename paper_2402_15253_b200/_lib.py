@@ -23,6 +23,7 @@ F_PULL_ALWAYS = 128
 F_RELABEL = 256
 F_NO_RELABEL = 512
 F_CLAMP_CAS = 1024
+F_PREFILTER = 2048
 
 K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel"]
 

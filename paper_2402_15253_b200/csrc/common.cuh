@@ -123,9 +123,12 @@ __device__ __forceinline__ int2 ld_stream_int2(const int2 *p, unsigned long long
 #define ld_cg_u32(p, pol) __ldcg(p)
 #endif
 
-// fire-and-forget global reduction (REDG), relaxed, device scope
+// fire-and-forget global reductions (REDG), relaxed, device scope
 __device__ __forceinline__ void red_add(int *p, int v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or(unsigned *p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Software grid barrier for persistent kernels launched cooperatively (all

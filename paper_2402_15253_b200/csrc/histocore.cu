@@ -83,6 +83,7 @@ struct HcArgs {
     int2 *S;               // update segments of C_t
     int2 *H;               // static hub segments (pull mode)
     unsigned *chg;         // [2][nwords] changed bitmaps
+    unsigned *capd;        // [nwords] cap-touched bitmap (UpdateHisto -> SumHisto)
     long long nwords;
     unsigned long long *fsz;  // [fsz_cap] per-round frontier sizes
     unsigned long long *rarcs;  // [fsz_cap] per-round arcs of C_t (stats)
@@ -92,7 +93,29 @@ struct HcArgs {
     int allow_pull;
     const shadow_t *nv16;  // neighbour-degree lookups of InitHisto (see init_val)
     const int *nv32;
+    // degree prefilter (push UpdateHisto): rows copied in descending order of
+    // the neighbours' degree bucket floor(log2 deg); a changed v with new
+    // estimate c scans only the prefix whose bucket may hold deg(u) > c
+    // (core[u] <= deg(u), so the rest can never pass the guard core[u] > c)
+    int prefilter;
+    int *ro;               // [2m] bucket-ordered copy of colidx
+    unsigned char *db;     // [n]  floor(log2(deg))
+    int *slen;             // [n]  scanned prefix of v's row for its latest change
 };
+
+// prefix of v's bucket-ordered row that UpdateHisto must scan after v's
+// estimate became c: entries with bucket >= floor(log2(c + 1)) (binary
+// search; buckets are non-increasing along the row)
+__device__ __forceinline__ int scan_len(const HcArgs &a, long long hb, int d, int c) {
+    if (!a.prefilter || d <= a.tn.a_max) return d;
+    const int bmin = 31 - __clz(c + 1);
+    int lo = 0, hi = d;  // first position with bucket < bmin
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((int)__ldg(a.db + __ldg(a.ro + hb + mid)) >= bmin) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -192,6 +215,7 @@ __global__ void hc_degree_kernel(HcArgs a) {
             a.oldc[v] = (int)d;  // round-0 estimate of every vertex
             a.core[v] = (int)d;
             set_c8(a, v, (int)d);
+            if (a.prefilter) a.db[v] = d > 0 ? (unsigned char)(31 - __clz((int)d)) : 0;
         }
         bool isB = valid && d > a.tn.a_max && d <= a.tn.b_max;
         bool isC = valid && d > a.tn.b_max;
@@ -206,6 +230,62 @@ __global__ void hc_degree_kernel(HcArgs a) {
             if (isC) a.BC[a.n - 1 - (long long)(base + __popc(m & ((1u << lane_id()) - 1)))] = v;
         }
         warp_append_segments(v, (valid && d > a.tn.seg) ? nseg_of(d, a.tn.seg) : 0, a.H, &a.ctl->nH);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// degree prefilter: counting sort of each class-B / class-C row by the
+// neighbours' degree bucket, descending (class-A rows are copied by init)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) hc_reorder_warp_kernel(HcArgs a) {
+    __shared__ int cnt[8][32];
+    const int wib = threadIdx.x >> 5, lane = lane_id();
+    int *c = cnt[wib];
+    const long long nB = (long long)a.ctl->nB;
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long idx = gw; idx < nB; idx += nw) {
+        int v = a.BC[idx];
+        long long hb = a.rp[v];
+        int d = (int)(a.rp[v + 1] - hb);
+        c[lane] = 0;
+        __syncwarp();
+        for (int e = lane; e < d; e += 32) atomicAdd(&c[31 - a.db[__ldg(a.ci + hb + e)]], 1);
+        __syncwarp();
+        int x = c[lane];
+        int incl = warp_incl_scan(x);
+        c[lane] = incl - x;
+        __syncwarp();
+        for (int e = lane; e < d; e += 32) {
+            int u = __ldg(a.ci + hb + e);
+            a.ro[hb + atomicAdd(&c[31 - a.db[u]], 1)] = u;
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(512) hc_reorder_cta_kernel(HcArgs a) {
+    __shared__ int c[32];
+    const long long nC = (long long)a.ctl->nC;
+    for (long long idx = blockIdx.x; idx < nC; idx += gridDim.x) {
+        int v = a.BC[a.n - 1 - idx];
+        long long hb = a.rp[v];
+        int d = (int)(a.rp[v + 1] - hb);
+        if (threadIdx.x < 32) c[threadIdx.x] = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < d; e += blockDim.x) atomicAdd(&c[31 - a.db[__ldg(a.ci + hb + e)]], 1);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int x = c[threadIdx.x];
+            int incl = warp_incl_scan(x);
+            c[threadIdx.x] = incl - x;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < d; e += blockDim.x) {
+            int u = __ldg(a.ci + hb + e);
+            a.ro[hb + atomicAdd(&c[31 - a.db[u]], 1)] = u;
+        }
+        __syncthreads();
     }
 }
 
@@ -247,7 +327,9 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
 #pragma unroll
             for (int b = 0; b < NB; b++) cnt[b] = 0;
             for (int e = 0; e < d; e++) {
-                int x = init_val(a, ld_stream(a.ci + hb + e, cold), d, hot);  // min(core[u], core[v])
+                int u = ld_stream(a.ci + hb + e, cold);
+                if (a.prefilter) a.ro[hb + e] = u;  // short rows: copied in order
+                int x = init_val(a, u, d, hot);     // min(core[u], core[v])
 #pragma unroll
                 for (int b = 0; b < NB; b++) cnt[b] += (x == b + 1);
             }
@@ -265,7 +347,10 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
                 else if (b == h) a.histo[hb + b - 1] = hs;
             }
             a.core[v] = h;
-            if (h < d) nseg = nseg_of(d, a.tn.seg);
+            if (h < d) {
+                a.slen[v] = d;  // d <= a_max: whole row
+                nseg = nseg_of(d, a.tn.seg);
+            }
         }
         if (nseg > 0) acc.note(a, 1, v, h, d);
         warp_append_segments(v, nseg, a.S, &a.ctl->nS[1]);
@@ -317,10 +402,17 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         }
         for (int b = 1 + lane; b <= h; b += 32) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
         __syncwarp();
-        int nseg = (h < d) ? nseg_of(d, a.tn.seg) : 0;
+        const bool changed = h < d;
+        int L = 0;
+        if (changed && lane == 0) L = scan_len(a, hb, d, h);
+        L = __shfl_sync(FULL, L, 0);
+        int nseg = nseg_of(L, a.tn.seg);
         if (lane == 0) {
             a.core[v] = h;
-            if (nseg) acc.note(a, 1, v, h, d);
+            if (changed) {
+                a.slen[v] = L;
+                acc.note(a, 1, v, h, d);
+            }
             st_slots += h;
         }
         if (nseg) {
@@ -398,15 +490,19 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
     } else {
         for (int b = 1 + tid; b <= h; b += nt) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
     }
-    int nseg = (h < d) ? nseg_of(d, a.tn.seg) : 0;
     if (tid == 0) {
+        const bool changed = h < d;
         a.core[v] = h;
-        if (nseg) {
+        int L = changed ? scan_len(a, hb, d, h) : 0;
+        int ns = nseg_of(L, a.tn.seg);
+        red[35] = ns;
+        if (changed) {
+            a.slen[v] = L;
             atomicAdd(&a.ctl->nF[1], 1ull);
             atomicAdd(&a.ctl->arcsC[1], (unsigned long long)d);
             atomicMin(&a.ctl->mincv[1], h);
             atomicOr(a.chg + a.nwords + (v >> 5), 1u << (v & 31));
-            red[34] = (int)atomicAdd(&a.ctl->nS[1], (unsigned long long)nseg);
+            if (ns) red[34] = (int)atomicAdd(&a.ctl->nS[1], (unsigned long long)ns);
         }
         if (STATS) {
             atomicAdd(&a.ctl->st_init_slots, (unsigned long long)(GLOBAL ? d : h));
@@ -414,6 +510,7 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
         }
     }
     __syncthreads();
+    const int nseg = red[35];
     if (nseg) {
         unsigned long long base = (unsigned)red[34];
         for (int s2 = tid; s2 < nseg; s2 += nt) a.S[base + s2] = make_int2(v, s2);
@@ -450,9 +547,25 @@ __global__ void hc_shadow_kernel(HcArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// one (v, u) bin move of UpdateHisto on u's histogram (hbu = rowptr[u] - 1):
-// returns true iff this call drove cnt(u) below core[u] (the push)
+// one (v, u) bin move of UpdateHisto on u's histogram (hbu = rowptr[u] - 1)
 // ---------------------------------------------------------------------------
+// Single-GPU rounds: every RMW is fire-and-forget (REDG).  A decrement of the
+// cap bin (the only way cnt(u) can drop) marks u in the
+// cap-touched bitmap; the next SumHisto phase keeps exactly the marked u with
+// cnt(u) < core[u] (Theorem 2) -- the same F_{t+1} as the
+// returned-value trigger of Alg 6, without any warp waiting on an atomic.
+__device__ __forceinline__ void bin_move_mark(const HcArgs &a, long long hbu, int u, int cu, int cv, int ov) {
+    if (ov >= cu) {
+        red_add(a.histo + hbu + cu, -1);
+        red_or(a.capd + (u >> 5), 1u << (u & 31));
+    } else {
+        red_add(a.histo + hbu + ov, -1);
+    }
+    red_add(a.histo + hbu + cv, 1);
+}
+
+// Sharded rounds (sh_update_kernel): the literal trigger -- returns true iff
+// this call drove cnt(u) below core[u] (old == core[u], exactly once)
 __device__ __forceinline__ bool bin_move(int *histo, long long hbu, int cu, int cv, int ov) {
     bool push = false;
     if (ov >= cu) {
@@ -490,10 +603,10 @@ __device__ __forceinline__ void append_pushes(const bool (&push)[U], const int (
 }
 
 // ---------------------------------------------------------------------------
-// UpdateHisto, push direction, round t: segments of C_t (count nS[t&1]) ->
-// F_{t+1} (count nF[(t+1)&1]).  Warps claim batches of 32 segments, scan
-// their lengths, and walk the concatenated arcs U*32 at a time (owner lane by
-// a 5-step shuffle binary search), U arcs in flight per lane.
+// UpdateHisto, push direction, round t: segments of C_t (count nS[t&1]).
+// Warps take batches of 32 segments, scan their lengths, and walk the
+// concatenated arcs U*32 at a time (owner lane by a 5-step shuffle binary
+// search), U arcs in flight per lane, no returning atomics.
 // ---------------------------------------------------------------------------
 template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
@@ -502,8 +615,7 @@ __device__ void update_phase(const HcArgs &a, int t) {
     const long long ns = (long long)ld_volatile(&a.ctl->nS[t & 1]);
     const long long nbatch = (ns + 31) >> 5;
     unsigned long long *wc = &a.ctl->wc[t & 1];
-    unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
-    long long st_arcs = 0, st_guard = 0, st_push = 0;
+    long long st_arcs = 0, st_guard = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -522,7 +634,8 @@ __device__ void update_phase(const HcArgs &a, int t) {
         int len = 0, cv = 0, ov = 0;
         if (i < ns) {
             int2 sg = ld_stream_int2(a.S + i, cold);
-            long long r0 = __ldg(a.rp + sg.x), r1 = __ldg(a.rp + sg.x + 1);
+            long long r0 = __ldg(a.rp + sg.x);
+            long long r1 = r0 + __ldcg(a.slen + sg.x);  // (prefiltered) prefix of the row
             b = r0 + (long long)sg.y * a.tn.seg;
             len = (int)min((long long)a.tn.seg, r1 - b);
             cv = __ldcg(a.core + sg.x);
@@ -530,10 +643,11 @@ __device__ void update_phase(const HcArgs &a, int t) {
         }
         int incl = warp_incl_scan(len);
         int excl = incl - len;
+        const int *rows = a.prefilter ? a.ro : a.ci;
         int total = __shfl_sync(FULL, incl, 31);
         for (int j0 = 0; j0 < total; j0 += 32 * U) {
             int u[U], cvo[U], ovo[U], cu[U];
-            bool ok[U], push[U];
+            bool ok[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 int j = j0 + q * 32 + lane;
@@ -549,7 +663,7 @@ __device__ void update_phase(const HcArgs &a, int t) {
                 cvo[q] = __shfl_sync(FULL, cv, lo);
                 ovo[q] = __shfl_sync(FULL, ov, lo);
                 ok[q] = j < total;
-                u[q] = ok[q] ? ld_stream(a.ci + eb + (j - ex), cold) : 0;
+                u[q] = ok[q] ? ld_stream(rows + eb + (j - ex), cold) : 0;
             }
 #pragma unroll
             for (int q = 0; q < U; q++) cu[q] = ok[q] ? core_of(a, u[q], hot) : 0;
@@ -557,25 +671,16 @@ __device__ void update_phase(const HcArgs &a, int t) {
             for (int q = 0; q < U; q++) {
                 if (STATS) st_arcs += ok[q];
                 ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
-                push[q] = false;
+                if (STATS) st_guard += ok[q];
             }
 #pragma unroll
             for (int q = 0; q < U; q++)
-                if (ok[q]) push[q] = bin_move(a.histo, __ldg(a.rp + u[q]) - 1, cu[q], cvo[q], ovo[q]);
-            append_pushes<U>(push, u, a.F, nF);
-            if (STATS) {
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    st_guard += ok[q];
-                    st_push += push[q];
-                }
-            }
+                if (ok[q]) bin_move_mark(a, __ldg(a.rp + u[q]) - 1, u[q], cu[q], cvo[q], ovo[q]);
         }
     }
     if (STATS) {
         stat_add(&a.ctl->st_arcs, st_arcs);
         stat_add(&a.ctl->st_guarded, st_guard);
-        stat_add(&a.ctl->st_pushes, st_push);
     }
 }
 
@@ -596,14 +701,11 @@ __device__ void pull_phase(const HcArgs &a, int t) {
     const long long nh = (long long)ld_volatile(&a.ctl->nH);
     const long long nbatch = nvb + ((nh + 31) >> 5);
     unsigned long long *wc = &a.ctl->wc[t & 1];
-    unsigned long long *nF = &a.ctl->nF[(t + 1) & 1];
-    long long st_arcs = 0, st_guard = 0, st_push = 0;
+    long long st_arcs = 0, st_guard = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long round = 0;; round++) {
-        // first batch static (warp id), the rest claimed dynamically (one
-        // atomic per 32 work items); small rounds cost no claim atomics
         long long bidx = gwarp;
         if (round > 0) {
             if (nbatch <= nwarps) break;
@@ -643,7 +745,7 @@ __device__ void pull_phase(const HcArgs &a, int t) {
         for (int j0 = 0; j0 < total; j0 += 32 * U) {
             int v[U], cuo[U], uo[U], cv[U];
             long long hbo[U];
-            bool ok[U], push[U];
+            bool ok[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 int j = j0 + q * 32 + lane;
@@ -671,36 +773,90 @@ __device__ void pull_phase(const HcArgs &a, int t) {
             for (int q = 0; q < U; q++) {
                 cv[q] = ok[q] ? core_of(a, v[q], hot) : 0;
                 ok[q] = ok[q] && cv[q] < cuo[q];
-                push[q] = false;
+                if (STATS) st_guard += ok[q];
             }
 #pragma unroll
             for (int q = 0; q < U; q++)
-                if (ok[q]) push[q] = bin_move(a.histo, hbo[q], cuo[q], cv[q], __ldcg(a.oldc + v[q]));
-            append_pushes<U>(push, uo, a.F, nF);
-            if (STATS) {
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    st_guard += ok[q];
-                    st_push += push[q];
-                }
-            }
+                if (ok[q]) bin_move_mark(a, hbo[q], uo[q], cuo[q], cv[q], __ldcg(a.oldc + v[q]));
         }
     }
     if (STATS) {
         stat_add(&a.ctl->st_arcs, st_arcs);
         stat_add(&a.ctl->st_guarded, st_guard);
-        stat_add(&a.ctl->st_pushes, st_push);
     }
 }
 
 // ---------------------------------------------------------------------------
-// SumHisto phase of round t: F_t (count nF[t&1]) -> core/oldcore/cap bin and
-// segments of C_t (count nS[t&1]).  Thread per vertex for the first 32 bins
-// of the descending walk, then warp-cooperative 32-bin chunks for long walks.
+// SumHisto of round t for one candidate vertex per lane (valid lanes): walk
+// k = core_old, core_old-1, ... adding bins until sum >= k, thread per vertex
+// for the first 32 bins, then warp-cooperative 32-bin chunks for long walks;
+// writes core/oldcore/cap bin and appends the vertex's UpdateHisto segments.
+// Warp-collective (all 32 lanes call).
 // ---------------------------------------------------------------------------
 template <bool STATS>
-__device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long nthreads) {
+__device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, int v, ChangeAcc &acc,
+                                          long long &st_bins, unsigned long long *nS) {
     const int lane = lane_id();
+    int cold = 0, k = 0, sum = 0;
+    long long hb = 0, d = 0;
+    bool done = true;
+    if (valid) {
+        cold = __ldcg(a.core + v);
+        hb = __ldg(a.rp + v) - 1;  // bin b at hb + b
+        d = __ldg(a.rp + v + 1) - hb - 1;
+        k = cold;
+        done = false;
+        for (int stp = 0; stp < 32; stp++) {
+            sum += __ldcg(a.histo + hb + k);
+            if (STATS) st_bins++;
+            if (sum >= k) { done = true; break; }
+            k--;
+        }
+    }
+    unsigned m = __ballot_sync(FULL, !done);
+    while (m) {
+        int L = __ffs(m) - 1;
+        m &= m - 1;
+        long long hbL = __shfl_sync(FULL, hb, L);
+        int kL = __shfl_sync(FULL, k, L);
+        int sL = __shfl_sync(FULL, sum, L);
+        int rk = 0, rs = 0;
+        for (;;) {
+            int kk = kL - lane;
+            int val = kk >= 1 ? __ldcg(a.histo + hbL + kk) : 0;
+            int incl = warp_incl_scan(val);
+            int s = sL + incl;
+            unsigned mm = __ballot_sync(FULL, kk >= 1 && s >= kk);
+            if (STATS) st_bins += (kk >= 1) ? 1 : 0;
+            if (mm) {
+                int f = __ffs(mm) - 1;
+                rk = kL - f;
+                rs = __shfl_sync(FULL, s, f);
+                break;
+            }
+            sL += __shfl_sync(FULL, incl, 31);
+            kL -= 32;
+        }
+        if (lane == L) { k = rk; sum = rs; }
+    }
+    int nseg = 0;
+    if (valid) {
+        a.core[v] = k;
+        set_c8(a, v, k);
+        a.oldc[v] = cold;
+        a.histo[hb + k] = sum;  // cap bin := cnt
+        int L = scan_len(a, hb + 1, (int)d, k);
+        a.slen[v] = L;
+        nseg = nseg_of(L, a.tn.seg);
+        acc.note(a, t, v, k, d);
+    }
+    warp_append_segments(v, nseg, a.S, nS);
+}
+
+// SumHisto of round t over an explicit frontier list F_t (count nF[t&1]):
+// the sharded path, whose UpdateHisto pushes with the returned-value trigger
+template <bool STATS>
+__device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long nthreads) {
     const long long nf = (long long)ld_volatile(&a.ctl->nF[t & 1]);
     unsigned long long *nS = &a.ctl->nS[t & 1];
     long long iters = (nf + nthreads - 1) / nthreads;
@@ -709,70 +865,57 @@ __device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long n
     for (long long it = 0; it < iters; it++) {
         long long i = it * nthreads + gthread;
         bool valid = i < nf;
-        int v = 0, cold = 0, k = 0, sum = 0;
-        long long hb = 0, d = 0;
-        bool done = true;
-        if (valid) {
-            v = __ldcg(a.F + i);
-            cold = __ldcg(a.core + v);
-            hb = __ldg(a.rp + v) - 1;  // bin b at hb + b
-            d = __ldg(a.rp + v + 1) - hb - 1;
-            k = cold;
-            done = false;
-            for (int stp = 0; stp < 32; stp++) {
-                sum += __ldcg(a.histo + hb + k);
-                if (STATS) st_bins++;
-                if (sum >= k) { done = true; break; }
-                k--;
-            }
-        }
-        unsigned m = __ballot_sync(FULL, !done);
-        while (m) {
-            int L = __ffs(m) - 1;
-            m &= m - 1;
-            long long hbL = __shfl_sync(FULL, hb, L);
-            int kL = __shfl_sync(FULL, k, L);
-            int sL = __shfl_sync(FULL, sum, L);
-            int rk = 0, rs = 0;
-            for (;;) {
-                int kk = kL - lane;
-                int val = kk >= 1 ? __ldcg(a.histo + hbL + kk) : 0;
-                int incl = warp_incl_scan(val);
-                int s = sL + incl;
-                unsigned mm = __ballot_sync(FULL, kk >= 1 && s >= kk);
-                if (STATS) st_bins += (kk >= 1) ? 1 : 0;
-                if (mm) {
-                    int f = __ffs(mm) - 1;
-                    rk = kL - f;
-                    rs = __shfl_sync(FULL, s, f);
-                    break;
-                }
-                sL += __shfl_sync(FULL, incl, 31);
-                kL -= 32;
-            }
-            if (lane == L) { k = rk; sum = rs; }
-        }
-        int nseg = 0;
-        if (valid) {
-            a.core[v] = k;
-            set_c8(a, v, k);
-            a.oldc[v] = cold;
-            a.histo[hb + k] = sum;  // cap bin := cnt
-            nseg = nseg_of(d, a.tn.seg);
-        }
-        if (valid) acc.note(a, t, v, k, d);
-        warp_append_segments(v, nseg, a.S, nS);
+        int v = valid ? __ldcg(a.F + i) : 0;
+        sum_lanes<STATS>(a, t, valid, v, acc, st_bins, nS);
     }
     acc.flush(a, t, nullptr);
     if (STATS) stat_add(&a.ctl->st_bins, st_bins);
 }
 
+// SumHisto of round t over the vertices marked in the cap-touched bitmap by
+// UpdateHisto(t-1): F_t = {marked u : cnt(u) < core[u]} (Theorem 2).  Each
+// lane owns one bitmap word (read and cleared); |F_t| -> nF[t&1].
+template <bool STATS>
+__device__ void collect_sum_phase(const HcArgs &a, int t) {
+    const int lane = lane_id();
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long *nS = &a.ctl->nS[t & 1];
+    long long st_bins = 0;
+    ChangeAcc acc;
+    for (long long wbase = gwarp * 32; wbase < a.nwords; wbase += nwarps * 32) {
+        long long wi = wbase + lane;
+        unsigned w = 0;
+        if (wi < a.nwords) {
+            w = __ldcg(a.capd + wi);
+            if (w) a.capd[wi] = 0u;
+        }
+        while (__any_sync(FULL, w != 0)) {
+            bool valid = false;
+            int v = 0;
+            if (w) {
+                v = (int)(wi * 32 + (__ffs(w) - 1));
+                w &= w - 1;
+                int cu = __ldcg(a.core + v);
+                valid = __ldcg(a.histo + __ldg(a.rp + v) + cu - 1) < cu;  // cnt < core
+            }
+            sum_lanes<STATS>(a, t, valid, v, acc, st_bins, nS);
+        }
+    }
+    acc.flush(a, t, &a.ctl->nF[t & 1]);
+    if (STATS) {
+        stat_add(&a.ctl->st_bins, st_bins);
+        stat_add(&a.ctl->st_pushes, acc.cnt);
+    }
+}
+
 // start-of-UpdateHisto(t) bookkeeping: reset round t+1's counters (unused
-// during this phase), clear round t+1's bitmap, pick push or pull
+// during this phase), clear round t+1's changed bitmap, pick push or pull
 __device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool leader, long long gthread,
                                                 long long nthreads, bool stats) {
     if (leader) {
         a.ctl->nS[(t + 1) & 1] = 0;
+        a.ctl->nF[(t + 1) & 1] = 0;
         a.ctl->wc[(t + 1) & 1] = 0;
         a.ctl->arcsC[(t + 1) & 1] = 0;
         a.ctl->mincv[(t + 1) & 1] = INT_MAX;
@@ -787,6 +930,7 @@ __device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool lea
 
 // ---------------------------------------------------------------------------
 // persistent cooperative kernel: all rounds t >= 1 with grid barriers
+//   UpdateHisto(t)  |barrier|  SumHisto(t+1) over the marked vertices  |barrier|
 // ---------------------------------------------------------------------------
 template <bool STATS>
 __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
@@ -803,16 +947,15 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
             update_phase<STATS>(a, t);
         }
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        collect_sum_phase<STATS>(a, t + 1);
+        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
         unsigned long long nf = ld_volatile(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
         if (leader) {
-            a.ctl->nF[t & 1] = 0;
             a.ctl->rounds++;
             if ((unsigned long long)t < a.fsz_cap) a.fsz[t] = nf;
             if (STATS) a.ctl->st_frontier += nf;
         }
-        sum_phase<STATS>(a, t + 1, gthread, nthreads);
-        grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
     }
 }
 
@@ -831,6 +974,12 @@ __global__ void __launch_bounds__(512, 2) hc_update_kernel(HcArgs a, int t, int 
     }
 }
 
+template <bool STATS>
+__global__ void __launch_bounds__(512, 2) hc_collect_sum_kernel(HcArgs a, int t) {
+    collect_sum_phase<STATS>(a, t);
+}
+
+// sharded rounds: SumHisto over the pushed frontier list
 template <bool STATS>
 __global__ void __launch_bounds__(512) hc_sum_kernel(HcArgs a, int t) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -857,7 +1006,7 @@ Tune hc_tune(uint32_t flags) {
 }
 
 struct HcLayout {
-    size_t ctl, fsz, rarcs, histo, c8, oldc, F, BC, S, H, chg, total;
+    size_t ctl, fsz, rarcs, histo, c8, oldc, F, BC, S, H, chg, ro, db, slen, capd, total;
     long long nwords, scap, hcap;
 };
 
@@ -879,6 +1028,10 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     L.S = b; b += align256(sizeof(int2) * (size_t)L.scap);
     L.H = b; b += align256(sizeof(int2) * (size_t)L.hcap);
     L.chg = b; b += align256(sizeof(unsigned) * 2 * (size_t)L.nwords);
+    L.ro = b; b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
+    L.db = b; b += align256((size_t)n);
+    L.slen = b; b += align256(sizeof(int) * (size_t)n);
+    L.capd = b; b += align256(sizeof(unsigned) * (size_t)L.nwords);
     L.total = b;
     return L;
 }
@@ -939,6 +1092,10 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.S = (int2 *)(p + L.S);
     a.H = (int2 *)(p + L.H);
     a.chg = (unsigned *)(p + L.chg);
+    a.ro = (int *)(p + L.ro);
+    a.db = (unsigned char *)(p + L.db);
+    a.slen = (int *)(p + L.slen);
+    a.capd = (unsigned *)(p + L.capd);
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)n; a.arcs = arcs; a.core = core; a.tn = tn;
     // Pull pays when push's remote histogram RMWs and shadow gathers miss L2,
@@ -947,6 +1104,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.allow_pull = (flags & PICO_F_PUSH_ONLY) ? 0 : (flags & PICO_F_PULL_ALWAYS) ? 1 : (n >= kPullMinN);
     a.nv16 = a.c8;
     a.nv32 = a.oldc;
+    a.prefilter = (flags & PICO_F_PREFILTER) ? 1 : 0;
 
     Timer tm{s, (flags & PICO_F_TIMING) != 0, {}};
     cudaError_t err;
@@ -954,6 +1112,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     hc.mincv[0] = hc.mincv[1] = INT_MAX;
     if ((err = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
     if ((err = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)L.nwords, s))) return err;
+    if ((err = cudaMemsetAsync(a.capd, 0, sizeof(unsigned) * (size_t)L.nwords, s))) return err;
 
     const int sms = dev.sms;
     long long launches = 0;
@@ -968,6 +1127,11 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     // H1-H3 (round 1)
     tm.start(PICO_K_INIT);
     {
+        if (a.prefilter) {  // bucket-ordered copies of the rows with deg > a_max
+            hc_reorder_warp_kernel<<<sms * 4, 256, 0, s>>>(a);
+            hc_reorder_cta_kernel<<<sms * 2, 512, 0, s>>>(a);
+            launches += 2;
+        }
         int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
         hc_init_small_kernel<STATS><<<std::max(blocks, 1), 256, 0, s>>>(a);
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
@@ -1011,7 +1175,10 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 tm.start(PICO_K_UPDATE);
                 hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t, pull);
                 tm.stop();
-                launches++;
+                tm.start(PICO_K_SUM);
+                hc_collect_sum_kernel<STATS><<<blocks, 512, 0, s>>>(a, t + 1);
+                tm.stop();
+                launches += 2;
                 unsigned long long nf = 0;
                 if ((err = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf),
                                            cudaMemcpyDeviceToHost, s)))
@@ -1020,11 +1187,6 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 if (nf == 0) break;
                 rounds++;
                 hsz.push_back(nf);
-                int sb = (int)std::min<long long>(((long long)nf + 511) / 512, (long long)sms * 4);
-                tm.start(PICO_K_SUM);
-                hc_sum_kernel<STATS><<<std::max(sb, 1), 512, 0, s>>>(a, t + 1);
-                tm.stop();
-                launches++;
             }
         } else {
             int occ = 0;
@@ -1296,9 +1458,14 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.S = (int2 *)(p + L.S);
     a.H = (int2 *)(p + L.H);
     a.chg = (unsigned *)(p + L.chg);
+    a.ro = (int *)(p + L.ro);
+    a.db = (unsigned char *)(p + L.db);
+    a.slen = (int *)(p + L.slen);
+    a.capd = (unsigned *)(p + L.capd);
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)nloc; a.arcs = h->arcs; a.tn = hc_tune(flags);
     a.allow_pull = 0;
+    a.prefilter = 0;  // the shard's UpdateHisto walks the CSC, not the rows
     p += align256(L.total);
     h->deg16g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
     h->csc_off = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));

@@ -25,7 +25,8 @@ def _variants(algo):
             pico.F_RELABEL, pico.F_RELABEL | pico.F_TINY_TILES | pico.F_STATS]
     if algo == "histocore":
         base += [pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
-                 pico.F_PULL_ALWAYS | pico.F_HOST_LOOP, pico.F_PUSH_ONLY | pico.F_HOST_LOOP]
+                 pico.F_PULL_ALWAYS | pico.F_HOST_LOOP, pico.F_PUSH_ONLY | pico.F_HOST_LOOP,
+                 pico.F_PREFILTER, pico.F_PREFILTER | pico.F_TINY_TILES]
     if algo == "peelone":
         base += [pico.F_CLAMP_SUB, pico.F_CLAMP_SUB | pico.F_HOST_LOOP, pico.F_CLAMP_SUB | pico.F_TINY_TILES,
                  pico.F_CLAMP_CAS, pico.F_CLAMP_CAS | pico.F_HOST_LOOP, pico.F_CLAMP_CAS | pico.F_TINY_TILES]
