@@ -131,6 +131,25 @@ __device__ __forceinline__ void red_or(unsigned *p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Block-uniform read of a control word other CTAs wrote before a barrier:
+// thread 0 loads it and broadcasts through shared memory, so a 300K-thread
+// grid issues one L2 request per CTA instead of one per thread to a single
+// address (which serialises on one L2 slice).  Block-collective.
+__device__ __forceinline__ unsigned long long bcast_u64(const unsigned long long *p) {
+    __shared__ unsigned long long s_u64;
+    __syncthreads();
+    if (threadIdx.x == 0) s_u64 = *reinterpret_cast<const volatile unsigned long long *>(p);
+    __syncthreads();
+    return s_u64;
+}
+__device__ __forceinline__ int bcast_i32(const int *p) {
+    __shared__ int s_i32;
+    __syncthreads();
+    if (threadIdx.x == 0) s_i32 = *reinterpret_cast<const volatile int *>(p);
+    __syncthreads();
+    return s_i32;
+}
+
 // Software grid barrier for persistent kernels launched cooperatively (all
 // CTAs co-resident).  Sense via a generation counter.
 __device__ __forceinline__ void grid_barrier(unsigned *arrive, unsigned *gen) {

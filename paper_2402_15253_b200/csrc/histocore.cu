@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) hc_reorder_warp_kernel(HcArgs a) {
     __shared__ int cnt[8][32];
     const int wib = threadIdx.x >> 5, lane = lane_id();
     int *c = cnt[wib];
-    const long long nB = (long long)a.ctl->nB;
+    const long long nB = (long long)bcast_u64(&a.ctl->nB);
     const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long idx = gw; idx < nB; idx += nw) {
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(256) hc_reorder_warp_kernel(HcArgs a) {
 
 __global__ void __launch_bounds__(512) hc_reorder_cta_kernel(HcArgs a) {
     __shared__ int c[32];
-    const long long nC = (long long)a.ctl->nC;
+    const long long nC = (long long)bcast_u64(&a.ctl->nC);
     for (long long idx = blockIdx.x; idx < nC; idx += gridDim.x) {
         int v = a.BC[a.n - 1 - idx];
         long long hb = a.rp[v];
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
     const int wib = threadIdx.x >> 5;
     const int lane = lane_id();
     int *bins = sh + wib * (a.tn.b_max + 1);
-    const long long nB = (long long)a.ctl->nB;
+    const long long nB = (long long)bcast_u64(&a.ctl->nB);
     const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     ChangeAcc acc;
@@ -522,7 +522,7 @@ template <bool STATS>
 __global__ void __launch_bounds__(512) hc_init_cta_kernel(HcArgs a) {
     extern __shared__ int bins[];
     __shared__ int red[40];
-    const long long nC = (long long)a.ctl->nC;
+    const long long nC = (long long)bcast_u64(&a.ctl->nC);
     for (long long idx = blockIdx.x; idx < nC; idx += gridDim.x) {
         int v = a.BC[a.n - 1 - idx];
         cta_init_vertex<false, STATS>(a, v, bins, red);
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(512) hc_init_cta_kernel(HcArgs a) {
 template <bool STATS>
 __global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
     __shared__ int red[40];
-    const long long nX = (long long)a.ctl->nX;
+    const long long nX = (long long)bcast_u64(&a.ctl->nX);
     for (long long idx = blockIdx.x; idx < nX; idx += gridDim.x) {
         int v = a.F[idx];
         cta_init_vertex<true, STATS>(a, v, nullptr, red);
@@ -612,7 +612,7 @@ template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
     constexpr int U = 4;
     const int lane = lane_id();
-    const long long ns = (long long)ld_volatile(&a.ctl->nS[t & 1]);
+    const long long ns = (long long)bcast_u64(&a.ctl->nS[t & 1]);
     const long long nbatch = (ns + 31) >> 5;
     unsigned long long *wc = &a.ctl->wc[t & 1];
     long long st_arcs = 0, st_guard = 0;
@@ -673,6 +673,8 @@ __device__ void update_phase(const HcArgs &a, int t) {
                 ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
                 if (STATS) st_guard += ok[q];
             }
+            // (fetching rowptr[u] speculatively alongside the shadow was
+            // measured slower: the extra L2 traffic outweighs the overlap)
 #pragma unroll
             for (int q = 0; q < U; q++)
                 if (ok[q]) bin_move_mark(a, __ldg(a.rp + u[q]) - 1, u[q], cu[q], cvo[q], ovo[q]);
@@ -696,9 +698,9 @@ __device__ void pull_phase(const HcArgs &a, int t) {
     constexpr int U = 4;
     const int lane = lane_id();
     const unsigned *chg = a.chg + (t & 1) * a.nwords;
-    const int mincv = ld_volatile(&a.ctl->mincv[t & 1]);
+    const int mincv = bcast_i32(&a.ctl->mincv[t & 1]);
     const long long nvb = ((long long)a.n + 31) >> 5;
-    const long long nh = (long long)ld_volatile(&a.ctl->nH);
+    const long long nh = (long long)bcast_u64(&a.ctl->nH);
     const long long nbatch = nvb + ((nh + 31) >> 5);
     unsigned long long *wc = &a.ctl->wc[t & 1];
     long long st_arcs = 0, st_guard = 0;
@@ -857,7 +859,7 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
 // the sharded path, whose UpdateHisto pushes with the returned-value trigger
 template <bool STATS>
 __device__ void sum_phase(const HcArgs &a, int t, long long gthread, long long nthreads) {
-    const long long nf = (long long)ld_volatile(&a.ctl->nF[t & 1]);
+    const long long nf = (long long)bcast_u64(&a.ctl->nF[t & 1]);
     unsigned long long *nS = &a.ctl->nS[t & 1];
     long long iters = (nf + nthreads - 1) / nthreads;
     long long st_bins = 0;
@@ -923,7 +925,7 @@ __device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool lea
     }
     unsigned *clr = a.chg + ((t + 1) & 1) * a.nwords;
     for (long long w = gthread; w < a.nwords; w += nthreads) clr[w] = 0u;
-    unsigned long long ac = ld_volatile(&a.ctl->arcsC[t & 1]);
+    unsigned long long ac = bcast_u64(&a.ctl->arcsC[t & 1]);
     if (leader && (unsigned long long)t < a.fsz_cap) a.rarcs[t] = ac;
     return a.allow_pull && ac * (unsigned long long)a.tn.pull_div >= (unsigned long long)a.arcs;
 }
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    if (ld_volatile(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
+    if (bcast_u64(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
     for (int t = 1;; t++) {
         bool pull = update_prologue(a, t, leader, gthread, nthreads, STATS);
         if (pull) {
@@ -949,7 +951,7 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
         collect_sum_phase<STATS>(a, t + 1);
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
-        unsigned long long nf = ld_volatile(&a.ctl->nF[(t + 1) & 1]);
+        unsigned long long nf = bcast_u64(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
         if (leader) {
             a.ctl->rounds++;

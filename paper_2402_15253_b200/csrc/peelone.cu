@@ -72,7 +72,7 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
 // scan of level k (parity p): alive[p] -> frontier entries in Q, alive[p^1]
 template <bool STATS>
 __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, long long nthreads) {
-    const long long na = (long long)ld_volatile(&a.ctl->nAlive[p]);
+    const long long na = (long long)bcast_u64(&a.ctl->nAlive[p]);
     const int *alive = p ? a.alive1 : a.alive0;
     int *next = p ? a.alive0 : a.alive1;
     long long iters = (na + nthreads - 1) / nthreads;
@@ -231,11 +231,11 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
     unsigned long long S = 0;  // global sub-round counter (claim counter parity)
     for (int L = 0;; L++) {
         const int p = L & 1;
-        long long na = (long long)ld_volatile(&c->nAlive[p]);
+        long long na = (long long)bcast_u64(&c->nAlive[p]);
         if (leader && L > 0) po_close_level(a, p ^ 1, kprev);
         if (na == 0) break;
-        k = max(k + 1, ld_volatile(&c->kminb[p]));
-        unsigned long long lstart = ld_volatile(&c->q_snap);
+        k = max(k + 1, bcast_i32(&c->kminb[p]));
+        unsigned long long lstart = bcast_u64(&c->q_snap);
         po_scan_phase<STATS>(a, k, p, gthread, nthreads);
         grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
         if (leader) {
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
         }
         unsigned long long lo = lstart;
         for (;;) {
-            unsigned long long hi = ld_volatile(&c->q_snap);
+            unsigned long long hi = bcast_u64(&c->q_snap);
             if (hi == lo) break;  // uniform: every CTA read the same snapshot
             po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
             grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
