@@ -61,7 +61,9 @@ int pico_shard_init(pico_shard_t h, const int32_t *deg_global, int64_t *changed_
 int pico_shard_pack(pico_shard_t h, int32_t *triples, int64_t cap, int64_t *count);
 
 /* Apply all ranks' triples (device int32 [3*total]) and run the local
- * SumHisto of the next round; *changed_local <- |C_{t+1} on this rank|. */
+ * SumHisto of the next round.  Asynchronous (stream-ordered, no host round
+ * trip) when changed_local is NULL; otherwise it waits and stores
+ * |C_{t+1} on this rank| there. */
 int pico_shard_apply(pico_shard_t h, const int32_t *triples, int64_t total, int64_t *changed_local);
 
 /* core_local (device int32 [nloc]) <- coreness of the owned vertices. */

@@ -411,11 +411,11 @@ int pico_shard_pack(pico_shard_t h, int32_t *triples, int64_t cap, int64_t *coun
 
 int pico_shard_apply(pico_shard_t h, const int32_t *triples, int64_t total, int64_t *changed_local) {
     g_last_error.clear();
-    if (!h || !changed_local || total < 0 || (total > 0 && !triples)) return fail(PICO_EINVAL, "bad argument");
+    if (!h || total < 0 || (total > 0 && !triples)) return fail(PICO_EINVAL, "bad argument");
     long long c = 0;
-    cudaError_t e = shard_apply(h->impl, triples, total, &c);
+    cudaError_t e = shard_apply(h->impl, triples, total, changed_local ? &c : nullptr);
     if (e) return cuda_fail(e, "shard apply");
-    *changed_local = c;
+    if (changed_local) *changed_local = c;
     return PICO_OK;
 }
 

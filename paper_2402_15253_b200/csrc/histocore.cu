@@ -1316,7 +1316,9 @@ __global__ void sh_csc_fill_kernel(const long long *rp, const int *ci, long long
 
 // C_t of this rank = segment-0 entries of S (init and SumHisto append one
 // (v, 0) per changed v) -> triples (v + vb, oldcore, core)
-__global__ void sh_pack_kernel(HcArgs a, long long ns, long long vb, int *out, unsigned long long *count) {
+__global__ void sh_pack_kernel(HcArgs a, const unsigned long long *ns_dev, long long vb, int *out,
+                               unsigned long long *count) {
+    const long long ns = (long long)bcast_u64(ns_dev);
     long long nt = (long long)gridDim.x * blockDim.x;
     long long iters = (ns + nt - 1) / nt;
     for (long long it = 0; it < iters; it++) {
@@ -1360,11 +1362,13 @@ __global__ void sh_segments_kernel(const int *tr, long long total, const long lo
 }
 
 // UpdateHisto of the received triples over the local CSC (push direction)
-__global__ void __launch_bounds__(512, 2) sh_update_kernel(HcArgs a, const int *tr, const int2 *TS, long long nts,
+__global__ void __launch_bounds__(512, 2) sh_update_kernel(HcArgs a, const int *tr, const int2 *TS,
+                                                           const unsigned long long *nts_dev,
                                                            const long long *csc_off, const int *csc_idx,
                                                            unsigned long long *nF) {
     constexpr int U = 4;
     const int lane = lane_id();
+    const long long nts = (long long)bcast_u64(nts_dev);  // no host round trip
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const unsigned long long hot = pol_last();
@@ -1550,14 +1554,8 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
 cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count) {
     cudaStream_t s = h->s;
     cudaError_t e;
-    unsigned long long ns = 0;
-    if ((e = cudaMemcpyAsync(&ns, &h->a.ctl->nS[h->t & 1], sizeof(ns), cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaMemsetAsync(h->cnt, 0, sizeof(unsigned long long), s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    if (ns) {
-        int blocks = (int)std::min<long long>(((long long)ns + 255) / 256, (long long)h->dev.sms * 16);
-        sh_pack_kernel<<<std::max(blocks, 1), 256, 0, s>>>(h->a, (long long)ns, h->vb, triples, h->cnt);
-    }
+    sh_pack_kernel<<<h->dev.sms * 4, 256, 0, s>>>(h->a, &h->a.ctl->nS[h->t & 1], h->vb, triples, h->cnt);
     unsigned long long c = 0;
     if ((e = cudaMemcpyAsync(&c, h->cnt, sizeof(c), cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
@@ -1577,28 +1575,25 @@ cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long
     if ((e = cudaMemsetAsync(nTS, 0, sizeof(unsigned long long), s))) return e;
     if ((e = cudaMemsetAsync(&a.ctl->nF[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
     if ((e = cudaMemsetAsync(&a.ctl->nS[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
-    unsigned long long nts = 0;
+    // stream-ordered, no host round trip: work counts are read on the device
+    // (the segment capacity n_global + 2m_local/seg bounds any round: the
+    // triples are distinct vertices)
     if (total > 0) {
         int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
         sh_segments_kernel<<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->csc_off, a.tn.seg, h->TS, nTS);
-        if ((e = cudaMemcpyAsync(&nts, nTS, sizeof(nts), cudaMemcpyDeviceToHost, s))) return e;
-        if ((e = cudaStreamSynchronize(s))) return e;
-        if ((long long)nts > h->tscap) return cudaErrorInvalidValue;
-        if (nts)
-            sh_update_kernel<<<sms * 2, 512, 0, s>>>(a, triples, h->TS, (long long)nts, h->csc_off, h->csc_idx,
-                                                     &a.ctl->nF[(t + 1) & 1]);
+        sh_update_kernel<<<sms * 2, 512, 0, s>>>(a, triples, h->TS, nTS, h->csc_off, h->csc_idx,
+                                                 &a.ctl->nF[(t + 1) & 1]);
     }
-    unsigned long long nf = 0;
-    if ((e = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf), cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    if (nf) {
-        int sb = (int)std::min<long long>(((long long)nf + 511) / 512, (long long)sms * 4);
-        hc_sum_kernel<false><<<std::max(sb, 1), 512, 0, s>>>(a, t + 1);
-    }
-    if ((e = cudaStreamSynchronize(s))) return e;
+    hc_sum_kernel<false><<<sms * 4, 512, 0, s>>>(a, t + 1);
+    if ((e = cudaGetLastError())) return e;
     h->t = t + 1;
-    *changed = (long long)nf;
-    return cudaGetLastError();
+    if (changed) {
+        unsigned long long nf = 0;
+        if ((e = cudaMemcpyAsync(&nf, &a.ctl->nF[(t + 1) & 1], sizeof(nf), cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        *changed = (long long)nf;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t shard_result(Shard *h, int *core_out) {

@@ -67,9 +67,9 @@ class TorchDistExchange:
     def allgather_counts(self, count: int, device) -> list[int]:
         import torch
         t = torch.tensor([count], dtype=torch.int64, device=device)
-        out = [torch.zeros_like(t) for _ in range(self.world)]
-        self.dist.all_gather(out, t, group=self.group)
-        return [int(x.item()) for x in out]
+        out = torch.empty(self.world, dtype=torch.int64, device=device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.tolist()  # one host read for all ranks
 
     def allgatherv(self, local, counts: list[int]):
         """Concatenation in rank order of every rank's `local[:counts[rank]]`
@@ -80,9 +80,11 @@ class TorchDistExchange:
             return local[:0]
         buf = torch.zeros(mx, dtype=local.dtype, device=local.device)
         buf[:counts[self.rank]] = local[:counts[self.rank]]
-        out = [torch.empty_like(buf) for _ in range(self.world)]
-        self.dist.all_gather(out, buf, group=self.group)
-        return torch.cat([o[:c] for o, c in zip(out, counts)])
+        out = torch.empty(self.world * mx, dtype=local.dtype, device=local.device)
+        self.dist.all_gather_into_tensor(out, buf, group=self.group)
+        if all(c == mx for c in counts):
+            return out
+        return torch.cat([out[r * mx:r * mx + c] for r, c in enumerate(counts)])
 
     def max_over_ranks(self, x: float, device) -> float:
         import torch
@@ -128,7 +130,11 @@ class DeviceShard:
         check(self.lib.pico_shard_pack(self.h, self.trip.data_ptr(), self.trip.numel() // 3, ctypes.byref(c)))
         return self.trip, c.value
 
-    def apply(self, triples, total: int) -> int:
+    def apply(self, triples, total: int, wait: bool = False):
+        """Asynchronous unless wait=True (then returns |C_{t+1}| of this rank)."""
+        if not wait:
+            check(self.lib.pico_shard_apply(self.h, triples.data_ptr() if total else None, total, None))
+            return None
         c = ctypes.c_int64()
         check(self.lib.pico_shard_apply(self.h, triples.data_ptr() if total else None, total, ctypes.byref(c)))
         return c.value
