@@ -151,6 +151,12 @@ typedef struct {
     /* optional caller-owned HOST array (same capacity) receiving, for
      * HistoCore, sum_{v in C_t} deg(v) for t = 1..rounds; may be NULL */
     int64_t *round_arcs;
+    /* optional caller-owned HOST array of 2 * frontier_sizes_cap entries
+     * receiving, for HistoCore rounds t = 1..rounds, the device time in ns
+     * (%globaltimer between grid barriers) of UpdateHisto(t) at [2(t-1)] and
+     * of the SumHisto that builds F_{t+1} at [2(t-1)+1]; may be NULL.  Filled
+     * by the persistent round kernel only (not PICO_F_HOST_LOOP). */
+    int64_t *round_ns;
 } pico_stats_t;
 
 /* The north-star entry point: coreness of every vertex, device buffers. */

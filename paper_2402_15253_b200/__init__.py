@@ -36,14 +36,16 @@ def workspace_bytes(n: int, m: int, algo="histocore", flags: int = 0) -> int:
 
 
 def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspace=None,
-             stats: Stats | None = None, frontier_sizes=None, round_arcs=None, stream=None):
+             stats: Stats | None = None, frontier_sizes=None, round_arcs=None, round_ns=None, stream=None):
     """Coreness of every vertex of a symmetric deduplicated CSR graph held in
     device memory (``pico_coreness_ex``).
 
     rowptr: int64 CUDA tensor [n+1]; colidx: int32 CUDA tensor [2m].
     Returns an int32 CUDA tensor [n].  ``stats`` (a :class:`Stats`) is filled
     in place; ``frontier_sizes`` an optional int64 numpy array receiving
-    |F_t| per round (HistoCore) or vertices per level (PeelOne).
+    |F_t| per round (HistoCore) or vertices per level (PeelOne);
+    ``round_arcs`` / ``round_ns`` (2 entries per round: UpdateHisto, SumHisto
+    device ns) optional int64 numpy arrays for HistoCore.
     """
     import torch
     lib = load()
@@ -74,6 +76,9 @@ def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspa
         if round_arcs is not None:
             assert round_arcs.size >= frontier_sizes.size
             st.round_arcs = round_arcs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        if round_ns is not None:
+            assert round_ns.size >= 2 * frontier_sizes.size
+            st.round_ns = round_ns.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
     with torch.cuda.device(rowptr.device):
         rc = lib.pico_coreness_ex(rowptr.data_ptr(), colidx.data_ptr() if arcs else None, n, m, _algo(algo),
                                   out.data_ptr() if n > 0 else None, ctypes.c_void_p(stream.cuda_stream), flags,

@@ -62,6 +62,7 @@ class Stats(ctypes.Structure):
         ("frontier_sizes", ctypes.POINTER(ctypes.c_int64)),
         ("frontier_sizes_cap", ctypes.c_int64),
         ("round_arcs", ctypes.POINTER(ctypes.c_int64)),
+        ("round_ns", ctypes.POINTER(ctypes.c_int64)),
     ]
 
     def to_dict(self) -> dict:

@@ -127,12 +127,13 @@ static cudaError_t dev_info(DevInfo *d) {
 
 static void reset_stats(pico_stats_t *st) {
     if (!st) return;
-    int64_t *fs = st->frontier_sizes, *ra = st->round_arcs;
+    int64_t *fs = st->frontier_sizes, *ra = st->round_arcs, *rn = st->round_ns;
     int64_t cap = st->frontier_sizes_cap;
     memset(st, 0, sizeof(*st));
     st->frontier_sizes = fs;
     st->frontier_sizes_cap = cap;
     st->round_arcs = ra;
+    st->round_ns = rn;
 }
 
 extern "C" {

@@ -13,6 +13,12 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // inclusive warp scan (sum) of a 32-bit value
 __device__ __forceinline__ int warp_incl_scan(int x) {
 #pragma unroll

@@ -2,10 +2,17 @@
 //
 // State in HBM:
 //   core[v]   int32   current estimate h_t(v) (= core_out; P:495 core <- deg)
-//   c8[v]     uint8   min(core[v], 255): an L2-resident shadow used by every
-//                     neighbour gather (exact below the saturation value; a
-//                     saturated entry falls back to core[v]; before the
-//                     rounds it holds min(deg(v), 255) for InitHisto)
+//   c8[v]     uint16  min(deg(v), 65535): the degree shadow InitHisto gathers
+//                     (a saturated entry falls back to oldc[v] = deg(v))
+//   rec[v]    uint32  the estimate record every round-loop gather reads:
+//                     low half  min(core[v], 65535),
+//                     high half min(oldcore[v], 65535) if v is in the current
+//                               changed set C_t, else the low half again,
+//                     so one 4-byte gather tells a pull arc whether its
+//                     neighbour changed, its new and its old estimate.  A
+//                     saturated half (65535) falls back to core/oldc and the
+//                     changed bitmap.  SumHisto writes the record of v in
+//                     C_{t+1}; the next SumHisto phase resets C_t's records.
 //   oldc[v]   int32   estimate before v's latest change (oldcore); during
 //                     init it holds deg(v), the round-0 estimate of every vertex
 //   histo     int32[2m], vertex v owns slots rowptr[v] + b - 1 for bins
@@ -48,26 +55,30 @@
 
 namespace pico {
 
-// build-time A/B knobs: shadow width (8 or 16 bits) and L2 eviction hints
-#ifndef PICO_SHADOW_BITS
-#define PICO_SHADOW_BITS 16
-#endif
+// build-time A/B knobs: L2 eviction hints
 #ifndef PICO_L2_HINTS
 #define PICO_L2_HINTS 0
 #endif
 // vertex count from which dense rounds may run UpdateHisto in the pull direction
-constexpr long long kPullMinN = 16ll << 20;
+#ifndef PICO_PULL_MIN_N
+#define PICO_PULL_MIN_N (16ll << 20)
+#endif
+constexpr long long kPullMinN = PICO_PULL_MIN_N;
 // arcs per UpdateHisto work item (segment of a changed row)
 #ifndef PICO_HC_SEG
 #define PICO_HC_SEG 64
 #endif
-#if PICO_SHADOW_BITS == 8
-typedef unsigned char shadow_t;
-constexpr unsigned SAT8 = 255;
-#else
 typedef unsigned short shadow_t;
-constexpr unsigned SAT8 = 65535;
+constexpr unsigned SAT8 = 65535;   // degree shadow saturation
+constexpr unsigned RSAT = 65535;   // estimate-record half saturation
+// pull-mode v-range passes: the record slice one pass gathers from
+#ifndef PICO_PASS_MB
+#define PICO_PASS_MB 32
 #endif
+constexpr int kMaxPass = 8;
+#ifndef PICO_PULL_AGG
+#define PICO_PULL_AGG 0            // warp-aggregate duplicate bin moves in pull mode
+#endif                             // (__match_any_sync; measured 1.4-3x slower)
 
 struct HcArgs {
     const long long *rp;   // rowptr [n+1]
@@ -75,7 +86,8 @@ struct HcArgs {
     int n;
     long long arcs;
     int *core;             // [n]  (core_out)
-    shadow_t *c8;          // [n]  saturated shadow of core
+    shadow_t *c8;          // [n]  saturated degree shadow (InitHisto)
+    unsigned *rec;         // [n]  estimate record (new16 | old16 << 16)
     int *oldc;             // [n]
     int *histo;            // [2m]
     int *F;                // [n]  frontier list; init: hub fallback list
@@ -87,6 +99,7 @@ struct HcArgs {
     long long nwords;
     unsigned long long *fsz;  // [fsz_cap] per-round frontier sizes
     unsigned long long *rarcs;  // [fsz_cap] per-round arcs of C_t (stats)
+    unsigned long long *rtime;  // [2 fsz_cap + 1] %globaltimer at the round kernel's barriers
     unsigned long long fsz_cap;
     Ctrl *ctl;
     Tune tn;
@@ -101,6 +114,13 @@ struct HcArgs {
     int *ro;               // [2m] bucket-ordered copy of colidx
     unsigned char *db;     // [n]  floor(log2(deg))
     int *slen;             // [n]  scanned prefix of v's row for its latest change
+    // pull rounds: the arcs (u, v) as an edge list bucketed by the v-range
+    // of the neighbour, bucket p = {v in [p*pw, (p+1)*pw)} at
+    // [boff[p], boff[p+1]) of psrc (= u) / pdst (= v); a pass over one
+    // bucket gathers the records of an L2-sized slice of the vertices
+    int npass, pw;
+    unsigned long long *boff;  // [kMaxPass + 1] bucket offsets
+    int *psrc, *pdst;
 };
 
 // prefix of v's bucket-ordered row that UpdateHisto must scan after v's
@@ -122,22 +142,31 @@ __device__ __forceinline__ int scan_len(const HcArgs &a, long long hb, int d, in
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int nseg_of(long long d, int seg) { return (int)((d + seg - 1) / seg); }
 
-// exact estimate of u through the 8-bit shadow (hot policy)
-__device__ __forceinline__ unsigned ld_shadow(const shadow_t *p, unsigned long long hot) {
+// 16-bit load (hot policy)
+__device__ __forceinline__ unsigned ld_shadow(const unsigned short *p, unsigned long long hot) {
 #if PICO_L2_HINTS
-#if PICO_SHADOW_BITS == 8
-    return ld_cg_u8(p, hot);
-#else
     return ld_cg_u16(p, hot);
-#endif
 #else
     return __ldcg(p);
 #endif
 }
 
+__device__ __forceinline__ unsigned pack_rec(int k, int old) {
+    return (unsigned)min(k, (int)RSAT) | ((unsigned)min(old, (int)RSAT) << 16);
+}
+
+__device__ __forceinline__ unsigned ld_rec(const unsigned *p, unsigned long long hot) {
+#if PICO_L2_HINTS
+    return ld_cg_u32(p, hot);
+#else
+    return __ldcg(p);
+#endif
+}
+
+// exact current estimate of u through its record
 __device__ __forceinline__ int core_of(const HcArgs &a, int u, unsigned long long hot) {
-    unsigned c = ld_shadow(a.c8 + u, hot);
-    return c == SAT8 ? __ldcg(a.core + u) : (int)c;
+    unsigned c = ld_rec(a.rec + u, hot) & 0xffffu;
+    return c == RSAT ? __ldcg(a.core + u) : (int)c;
 }
 
 __device__ __forceinline__ void set_c8(const HcArgs &a, int v, int k) {
@@ -539,11 +568,104 @@ __global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
     }
 }
 
-// after init: the shadow switches from degrees to the round-1 estimates
+// after init: estimate records of round 1 (C_1 = {v : h_1(v) < deg(v)},
+// oldcore = deg for its members)
 __global__ void hc_shadow_kernel(HcArgs a) {
     long long nthreads = (long long)gridDim.x * blockDim.x;
-    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += nthreads)
-        set_c8(a, (int)v, a.core[v]);
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += nthreads) {
+        int k = a.core[v], d = a.oldc[v];
+        a.rec[v] = pack_rec(k, d);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Edge list of the pull rounds, bucketed by the neighbour's v-range, in CSR
+// order inside each bucket: work batches (32 short rows, then 32 static hub
+// segments) count their arcs per bucket, one exclusive scan over the
+// bucket-major count matrix gives every (bucket, batch) its output offset,
+// and the batches write their (u, v) pairs in row order.
+// ---------------------------------------------------------------------------
+// lane's arc range of edge-list batch bidx (short rows, then hub segments)
+__device__ __forceinline__ void el_batch(const HcArgs &a, long long bidx, long long nvb, long long nh, int &uu,
+                                         long long &b, int &len) {
+    const int lane = lane_id();
+    uu = 0; b = 0; len = 0;
+    if (bidx < nvb) {
+        long long v = bidx * 32 + lane;
+        if (v < a.n) {
+            long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+            if (r1 - r0 <= a.tn.seg) { uu = (int)v; b = r0; len = (int)(r1 - r0); }
+        }
+    } else {
+        long long i = (bidx - nvb) * 32 + lane;
+        if (i < nh) {
+            int2 sg = a.H[i];
+            long long r0 = __ldg(a.rp + sg.x), r1 = __ldg(a.rp + sg.x + 1);
+            uu = sg.x;
+            b = r0 + (long long)sg.y * a.tn.seg;
+            len = (int)min((long long)a.tn.seg, r1 - b);
+        }
+    }
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(256) hc_edgelist_kernel(HcArgs a, long long nbcap, unsigned long long *cnt) {
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1;
+    const long long nvb = ((long long)a.n + 31) >> 5;
+    const long long nh = (long long)bcast_u64(&a.ctl->nH);
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long bidx = gw; bidx < nbcap; bidx += nw) {
+        int uu, len;
+        long long b;
+        el_batch(a, bidx, nvb, nh, uu, b, len);
+        int incl = warp_incl_scan(len);
+        int excl = incl - len;
+        int total = __shfl_sync(FULL, incl, 31);
+        unsigned long long cur[kMaxPass];
+#pragma unroll
+        for (int q = 0; q < kMaxPass; q++) cur[q] = FILL && q < a.npass ? cnt[(long long)q * nbcap + bidx] : 0;
+        for (int j0 = 0; j0 < total; j0 += 32) {
+            int j = j0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                int cand = lo + step;
+                int ex = __shfl_sync(FULL, excl, cand & 31);
+                if (cand < 32 && ex <= j) lo = cand;
+            }
+            long long eb = __shfl_sync(FULL, b, lo);
+            int ex = __shfl_sync(FULL, excl, lo);
+            int uo = __shfl_sync(FULL, uu, lo);
+            int v = j < total ? __ldg(a.ci + eb + (j - ex)) : 0;
+            int p = j < total ? v / a.pw : -1;
+#pragma unroll
+            for (int q = 0; q < kMaxPass; q++) {
+                if (q >= a.npass) break;
+                unsigned m = __ballot_sync(FULL, p == q);
+                if (FILL && p == q) {
+                    unsigned long long w = cur[q] + __popc(m & lt);
+                    a.psrc[w] = uo;
+                    a.pdst[w] = v;
+                }
+                cur[q] += __popc(m);
+            }
+        }
+        if (!FILL && lane < a.npass) {
+            unsigned long long c = 0;
+#pragma unroll
+            for (int q = 0; q < kMaxPass; q++)
+                if (q == lane) c = cur[q];
+            cnt[(long long)lane * nbcap + bidx] = c;
+        }
+    }
+}
+
+// bucket offsets from the scanned count matrix
+__global__ void hc_edgelist_offsets_kernel(HcArgs a, long long nbcap, const unsigned long long *off) {
+    if (threadIdx.x <= kMaxPass)
+        a.boff[threadIdx.x] = (int)threadIdx.x < a.npass ? off[(long long)threadIdx.x * nbcap] : (unsigned long long)a.arcs;
 }
 
 // ---------------------------------------------------------------------------
@@ -603,6 +725,48 @@ __device__ __forceinline__ void append_pushes(const bool (&push)[U], const int (
 }
 
 // ---------------------------------------------------------------------------
+// Arc stream of one warp batch: lane L owns the arc range [b_L, b_L + len_L)
+// (a row or a row segment); the concatenated ranges are walked 32*U arcs at a
+// time.  ArcStep holds, for each of a lane's U arcs, its owner lane and its
+// neighbour id (-1 past the end).  fetch() issues the colidx loads of a step
+// (owner = max lane with excl <= j, a 5-step shuffle binary search), so the
+// caller can fetch step i+1 before it waits on the gathers of step i.
+// Warp-collective.
+// ---------------------------------------------------------------------------
+#ifndef PICO_ARC_U
+#define PICO_ARC_U 4
+#endif
+#ifndef PICO_ARC_PF
+#define PICO_ARC_PF 1
+#endif
+template <int U>
+struct ArcStep {
+    int lo[U];
+    int v[U];
+};
+
+template <int U>
+__device__ __forceinline__ void arc_fetch(ArcStep<U> &st, int j0, int total, int excl, long long b,
+                                          const int *rows, unsigned long long cold) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        int j = j0 + q * 32 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            int cand = lo + step;
+            int ex = __shfl_sync(FULL, excl, cand & 31);
+            if (cand < 32 && ex <= j) lo = cand;
+        }
+        long long eb = __shfl_sync(FULL, b, lo);
+        int ex = __shfl_sync(FULL, excl, lo);
+        st.lo[q] = lo;
+        st.v[q] = j < total ? ld_stream(rows + eb + (j - ex), cold) : -1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // UpdateHisto, push direction, round t: segments of C_t (count nS[t&1]).
 // Warps take batches of 32 segments, scan their lengths, and walk the
 // concatenated arcs U*32 at a time (owner lane by a 5-step shuffle binary
@@ -610,7 +774,6 @@ __device__ __forceinline__ void append_pushes(const bool (&push)[U], const int (
 // ---------------------------------------------------------------------------
 template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
-    constexpr int U = 4;
     const int lane = lane_id();
     const long long ns = (long long)bcast_u64(&a.ctl->nS[t & 1]);
     const long long nbatch = (ns + 31) >> 5;
@@ -645,39 +808,32 @@ __device__ void update_phase(const HcArgs &a, int t) {
         int excl = incl - len;
         const int *rows = a.prefilter ? a.ro : a.ci;
         int total = __shfl_sync(FULL, incl, 31);
-        for (int j0 = 0; j0 < total; j0 += 32 * U) {
-            int u[U], cvo[U], ovo[U], cu[U];
-            bool ok[U];
+        constexpr int UA = PICO_ARC_U;
+        ArcStep<UA> nx;
+        if (total > 0) arc_fetch<UA>(nx, 0, total, excl, b, rows, cold);
+        for (int j0 = 0; j0 < total; j0 += 32 * UA) {
+            ArcStep<UA> cur = nx;
+            if (PICO_ARC_PF && j0 + 32 * UA < total) arc_fetch<UA>(nx, j0 + 32 * UA, total, excl, b, rows, cold);
+            int cu[UA];
 #pragma unroll
-            for (int q = 0; q < U; q++) {
-                int j = j0 + q * 32 + lane;
-                int lo = 0;  // owner = max lane with excl <= j
+            for (int q = 0; q < UA; q++) cu[q] = cur.v[q] >= 0 ? core_of(a, cur.v[q], hot) : 0;
+            int cvo[UA], ovo[UA];
+            long long hb[UA];
+            // all histogram bases are loaded before the first RED (the REDs'
+            // memory clobber would otherwise serialise load -> RED -> load)
 #pragma unroll
-                for (int step = 16; step >= 1; step >>= 1) {
-                    int cand = lo + step;
-                    int ex = __shfl_sync(FULL, excl, cand & 31);
-                    if (cand < 32 && ex <= j) lo = cand;
-                }
-                long long eb = __shfl_sync(FULL, b, lo);
-                int ex = __shfl_sync(FULL, excl, lo);
-                cvo[q] = __shfl_sync(FULL, cv, lo);
-                ovo[q] = __shfl_sync(FULL, ov, lo);
-                ok[q] = j < total;
-                u[q] = ok[q] ? ld_stream(rows + eb + (j - ex), cold) : 0;
+            for (int q = 0; q < UA; q++) {
+                cvo[q] = __shfl_sync(FULL, cv, cur.lo[q]);
+                ovo[q] = __shfl_sync(FULL, ov, cur.lo[q]);
+                if (STATS) st_arcs += cur.v[q] >= 0;
+                bool g = cur.v[q] >= 0 && cu[q] > cvo[q];  // N1/N3 neighbour
+                if (STATS) st_guard += g;
+                hb[q] = g ? __ldg(a.rp + cur.v[q]) - 1 : LLONG_MIN;  // rowptr[0] - 1 = -1 is valid
             }
 #pragma unroll
-            for (int q = 0; q < U; q++) cu[q] = ok[q] ? core_of(a, u[q], hot) : 0;
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                if (STATS) st_arcs += ok[q];
-                ok[q] = ok[q] && cu[q] > cvo[q];  // N1/N3 neighbour
-                if (STATS) st_guard += ok[q];
-            }
-            // (fetching rowptr[u] speculatively alongside the shadow was
-            // measured slower: the extra L2 traffic outweighs the overlap)
-#pragma unroll
-            for (int q = 0; q < U; q++)
-                if (ok[q]) bin_move_mark(a, __ldg(a.rp + u[q]) - 1, u[q], cu[q], cvo[q], ovo[q]);
+            for (int q = 0; q < UA; q++)
+                if (hb[q] != LLONG_MIN) bin_move_mark(a, hb[q], cur.v[q], cu[q], cvo[q], ovo[q]);
+            if (!PICO_ARC_PF && j0 + 32 * UA < total) arc_fetch<UA>(nx, j0 + 32 * UA, total, excl, b, rows, cold);
         }
     }
     if (STATS) {
@@ -687,101 +843,78 @@ __device__ void update_phase(const HcArgs &a, int t) {
 }
 
 // ---------------------------------------------------------------------------
-// UpdateHisto, pull direction, round t (dense rounds).  Work items: batches
-// of 32 consecutive vertices whose rows are short (deg <= seg; their arcs are
-// one contiguous colidx range) and batches of 32 static hub segments.  A row
-// u is streamed iff core[u] > min core_t(C_t); each arc (u, v) tests v in the
-// changed bitmap and applies the (v, u) bin move to u's own histogram.
+// UpdateHisto, pull direction (dense rounds), over the bucketed edge list:
+// for each v-range bucket in turn every warp streams a contiguous slice of
+// its (u, v) pairs; arc (u, v) applies the (v, u) bin move of a changed v
+// with core[v] < core[u] to u's own histogram.  Consecutive lanes mostly
+// share u, so core[u] / rowptr[u] loads and the bin moves coalesce; the one
+// random access per arc is the 4-byte record of v, inside the bucket's
+// L2-sized vertex slice.  No owner search, no per-row bookkeeping.
 // ---------------------------------------------------------------------------
 template <bool STATS>
-__device__ void pull_phase(const HcArgs &a, int t) {
-    constexpr int U = 4;
+__device__ void coo_pull_phase(const HcArgs &a, int t) {
+    constexpr int UA = PICO_ARC_U;
     const int lane = lane_id();
     const unsigned *chg = a.chg + (t & 1) * a.nwords;
-    const int mincv = bcast_i32(&a.ctl->mincv[t & 1]);
-    const long long nvb = ((long long)a.n + 31) >> 5;
-    const long long nh = (long long)bcast_u64(&a.ctl->nH);
-    const long long nbatch = nvb + ((nh + 31) >> 5);
-    unsigned long long *wc = &a.ctl->wc[t & 1];
     long long st_arcs = 0, st_guard = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long round = 0;; round++) {
-        long long bidx = gwarp;
-        if (round > 0) {
-            if (nbatch <= nwarps) break;
-            if (lane == 0) bidx = nwarps + (long long)atomicAdd(wc, 1ull);
-            bidx = __shfl_sync(FULL, bidx, 0);
+    __shared__ unsigned long long s_off[kMaxPass + 1];
+    __syncthreads();
+    if (threadIdx.x <= kMaxPass) s_off[threadIdx.x] = ld_volatile(a.boff + threadIdx.x);
+    __syncthreads();
+    for (int p = 0; p < a.npass; p++) {
+    // static contiguous slices of bucket p, whole 32*UA steps
+    const long long bb = (long long)s_off[p], be = (long long)s_off[p + 1];
+    const long long steps = (be - bb + 32 * UA - 1) / (32 * UA);
+    const long long s0 = steps * gwarp / nwarps, s1 = steps * (gwarp + 1) / nwarps;
+    for (long long st = s0; st < s1; st++) {
+        const long long e0 = bb + st * (32 * UA);
+        int u[UA], v[UA];
+        unsigned ru[UA], rv[UA];
+        long long hb[UA];
+#pragma unroll
+        for (int q = 0; q < UA; q++) {
+            long long e = e0 + q * 32 + lane;
+            bool ok = e < be;
+            u[q] = ok ? ld_stream(a.psrc + e, cold) : -1;
+            v[q] = ok ? ld_stream(a.pdst + e, cold) : 0;
         }
-        if (bidx >= nbatch) break;
-        long long b = 0;
-        int len = 0, cu = 0, uu = 0;
-        if (bidx < nvb) {
-            long long v = bidx * 32 + lane;
-            if (v < a.n) {
-                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-                uu = (int)v;
-                if (r1 > r0 && r1 - r0 <= a.tn.seg) {
-                    cu = core_of(a, uu, hot);
-                    if (cu > mincv) { b = r0; len = (int)(r1 - r0); }
-                }
-            }
-        } else {
-            long long i = (bidx - nvb) * 32 + lane;
-            if (i < nh) {
-                int2 sg = ld_stream_int2(a.H + i, cold);
-                uu = sg.x;
-                cu = core_of(a, uu, hot);
-                if (cu > mincv) {
-                    long long r0 = __ldg(a.rp + uu), r1 = __ldg(a.rp + uu + 1);
-                    b = r0 + (long long)sg.y * a.tn.seg;
-                    len = (int)min((long long)a.tn.seg, r1 - b);
-                }
-            }
+#pragma unroll
+        for (int q = 0; q < UA; q++) {
+            ru[q] = u[q] >= 0 ? ld_rec(a.rec + u[q], hot) : 0u;
+            rv[q] = u[q] >= 0 ? ld_rec(a.rec + v[q], hot) : 0u;
+            hb[q] = u[q] >= 0 ? __ldg(a.rp + u[q]) - 1 : 0;
         }
-        long long hbu = len ? __ldg(a.rp + uu) - 1 : 0;
-        int incl = warp_incl_scan(len);
-        int excl = incl - len;
-        int total = __shfl_sync(FULL, incl, 31);
-        for (int j0 = 0; j0 < total; j0 += 32 * U) {
-            int v[U], cuo[U], uo[U], cv[U];
-            long long hbo[U];
-            bool ok[U];
 #pragma unroll
-            for (int q = 0; q < U; q++) {
-                int j = j0 + q * 32 + lane;
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step >= 1; step >>= 1) {
-                    int cand = lo + step;
-                    int ex = __shfl_sync(FULL, excl, cand & 31);
-                    if (cand < 32 && ex <= j) lo = cand;
-                }
-                long long eb = __shfl_sync(FULL, b, lo);
-                int ex = __shfl_sync(FULL, excl, lo);
-                cuo[q] = __shfl_sync(FULL, cu, lo);
-                uo[q] = __shfl_sync(FULL, uu, lo);
-                hbo[q] = __shfl_sync(FULL, hbu, lo);
-                ok[q] = j < total;
-                v[q] = ok[q] ? ld_stream(a.ci + eb + (j - ex), cold) : 0;
+        for (int q = 0; q < UA; q++) {
+            const bool ok = u[q] >= 0;
+            if (STATS) st_arcs += ok;
+            int cu = (int)(ru[q] & 0xffffu);
+            if (ok && cu == (int)RSAT) cu = __ldcg(a.core + u[q]);
+            int nlo = (int)(rv[q] & 0xffffu), nhi = (int)(rv[q] >> 16);
+            int cv = nlo, ov = nhi;
+            bool ch = nlo != nhi;  // exact while the new half is unsaturated
+            if (ok && nlo == (int)RSAT) {  // estimate >= 65535: full arrays
+                ch = (__ldcg(chg + (v[q] >> 5)) >> (v[q] & 31)) & 1u;
+                cv = __ldcg(a.core + v[q]);
+                ov = ch ? __ldcg(a.oldc + v[q]) : cv;
+            } else if (ok && ch && nhi == (int)RSAT && cu > (int)RSAT) {
+                ov = __ldcg(a.oldc + v[q]);  // saturated old half, needed exactly
             }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                if (STATS) st_arcs += ok[q];
-                ok[q] = ok[q] && ((ld_cg_u32(chg + (v[q] >> 5), hot) >> (v[q] & 31)) & 1u);
+            bool g = ok && ch && cv < cu;  // N1/N3 neighbour
+            if (STATS) st_guard += g;
+            if (g) {
+                // source bin min(oldcore[v], core[u]): the cap bin iff oldcore[v] >= core[u]
+                const bool capdec = ov >= cu;
+                red_add(a.histo + hb[q] + (capdec ? cu : ov), -1);
+                if (capdec) red_or(a.capd + (u[q] >> 5), 1u << (u[q] & 31));
+                red_add(a.histo + hb[q] + cv, 1);
             }
-#pragma unroll
-            for (int q = 0; q < U; q++) {
-                cv[q] = ok[q] ? core_of(a, v[q], hot) : 0;
-                ok[q] = ok[q] && cv[q] < cuo[q];
-                if (STATS) st_guard += ok[q];
-            }
-#pragma unroll
-            for (int q = 0; q < U; q++)
-                if (ok[q]) bin_move_mark(a, hbo[q], uo[q], cuo[q], cv[q], __ldcg(a.oldc + v[q]));
         }
     }
+    }  // buckets
     if (STATS) {
         stat_add(&a.ctl->st_arcs, st_arcs);
         stat_add(&a.ctl->st_guarded, st_guard);
@@ -844,7 +977,7 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
     int nseg = 0;
     if (valid) {
         a.core[v] = k;
-        set_c8(a, v, k);
+        a.rec[v] = pack_rec(k, cold);
         a.oldc[v] = cold;
         a.histo[hb + k] = sum;  // cap bin := cnt
         int L = scan_len(a, hb + 1, (int)d, k);
@@ -883,6 +1016,7 @@ __device__ void collect_sum_phase(const HcArgs &a, int t) {
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     unsigned long long *nS = &a.ctl->nS[t & 1];
+    const unsigned *chgp = a.chg + ((t - 1) & 1) * a.nwords;  // C_{t-1}
     long long st_bins = 0;
     ChangeAcc acc;
     for (long long wbase = gwarp * 32; wbase < a.nwords; wbase += nwarps * 32) {
@@ -891,6 +1025,16 @@ __device__ void collect_sum_phase(const HcArgs &a, int t) {
         if (wi < a.nwords) {
             w = __ldcg(a.capd + wi);
             if (w) a.capd[wi] = 0u;
+            // C_{t-1}'s records stop flagging a change (old byte := new byte);
+            // the same lane then writes the records of F_t in this word, so
+            // the reset never overtakes a newer record
+            unsigned cw = __ldcg(chgp + wi);
+            while (cw) {
+                int v = (int)(wi * 32 + (__ffs(cw) - 1));
+                cw &= cw - 1;
+                int c = __ldcg(a.core + v);
+                a.rec[v] = pack_rec(c, c);
+            }
         }
         while (__any_sync(FULL, w != 0)) {
             bool valid = false;
@@ -940,17 +1084,20 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     if (bcast_u64(&a.ctl->nS[1]) == 0) return;  // C_1 empty: l2 = 0 (uniform)
+    if (leader) a.rtime[0] = globaltimer();
     for (int t = 1;; t++) {
         bool pull = update_prologue(a, t, leader, gthread, nthreads, STATS);
         if (pull) {
             if (STATS && leader) a.ctl->st_pull++;
-            pull_phase<STATS>(a, t);
+            coo_pull_phase<STATS>(a, t);
         } else {
             update_phase<STATS>(a, t);
         }
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        if (leader && (unsigned long long)t < a.fsz_cap) a.rtime[2 * t - 1] = globaltimer();
         collect_sum_phase<STATS>(a, t + 1);
         grid_barrier(&a.ctl->bar_arrive, &a.ctl->bar_gen);
+        if (leader && (unsigned long long)t < a.fsz_cap) a.rtime[2 * t] = globaltimer();
         unsigned long long nf = bcast_u64(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
         if (leader) {
@@ -970,7 +1117,7 @@ __global__ void __launch_bounds__(512, 2) hc_update_kernel(HcArgs a, int t, int 
     update_prologue(a, t, leader, gthread, nthreads, STATS);
     if (pull) {
         if (STATS && leader) a.ctl->st_pull++;
-        pull_phase<STATS>(a, t);
+        coo_pull_phase<STATS>(a, t);
     } else {
         update_phase<STATS>(a, t);
     }
@@ -1002,19 +1149,39 @@ Tune hc_tune(uint32_t flags) {
     } else {
         t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = PICO_HC_SEG;
     }
-    t.pull_div = 8;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
+#ifndef PICO_PULL_DIV
+#define PICO_PULL_DIV 8
+#endif
+    t.pull_div = PICO_PULL_DIV;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
     if (flags & PICO_F_PULL_ALWAYS) t.pull_div = 1 << 30;
     return t;
 }
 
+// whether dense rounds may pull, and into how many v-range passes
+static bool hc_allow_pull(long long n, uint32_t flags) {
+    return (flags & PICO_F_PUSH_ONLY) ? false : (flags & PICO_F_PULL_ALWAYS) ? true : (n >= kPullMinN);
+}
+
+static int hc_npass(long long n, uint32_t flags) {
+    if (!hc_allow_pull(n, flags) || n < 2) return 1;
+    if (flags & PICO_F_TINY_TILES) return (int)std::min<long long>(3, n);  // exercise the passes
+    long long per = (long long)PICO_PASS_MB << 20;
+    long long np = (4 * n + per - 1) / per;  // 4-byte records per pass <= PICO_PASS_MB
+    return (int)std::max(1ll, std::min<long long>(np, kMaxPass));
+}
+
 struct HcLayout {
-    size_t ctl, fsz, rarcs, histo, c8, oldc, F, BC, S, H, chg, ro, db, slen, capd, total;
-    long long nwords, scap, hcap;
+    size_t ctl, fsz, rarcs, rtime, histo, c8, rec, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
+        elc, elt, total;
+    long long nwords, scap, hcap, nbcap;
+    size_t eltb;
+    int npass;
 };
 
 static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     Tune tn = hc_tune(flags);
     HcLayout L;
+    L.npass = hc_npass(n, flags);
     L.nwords = (n + 31) / 32;
     L.scap = n + arcs / tn.seg + 64;
     L.hcap = 2 * (arcs / tn.seg) + 64;
@@ -1022,18 +1189,32 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     L.ctl = b; b += align256(sizeof(Ctrl));
     L.fsz = b; b += align256(sizeof(unsigned long long) * kFszCap);
     L.rarcs = b; b += align256(sizeof(unsigned long long) * kFszCap);
+    L.rtime = b; b += align256(sizeof(unsigned long long) * (2 * kFszCap + 1));
     L.histo = b; b += align256(sizeof(int) * (size_t)arcs);
     L.c8 = b; b += align256(sizeof(shadow_t) * (size_t)n);
+    L.rec = b; b += align256(sizeof(unsigned) * (size_t)n);
     L.oldc = b; b += align256(sizeof(int) * (size_t)n);
     L.F = b; b += align256(sizeof(int) * (size_t)n);
     L.BC = b; b += align256(sizeof(int) * (size_t)n);
     L.S = b; b += align256(sizeof(int2) * (size_t)L.scap);
     L.H = b; b += align256(sizeof(int2) * (size_t)L.hcap);
     L.chg = b; b += align256(sizeof(unsigned) * 2 * (size_t)L.nwords);
-    L.ro = b; b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
+    L.ro = b; b += align256(sizeof(int) * (size_t)((flags & PICO_F_PREFILTER) ? std::max(arcs, 1ll) : 1));
     L.db = b; b += align256((size_t)n);
     L.slen = b; b += align256(sizeof(int) * (size_t)n);
     L.capd = b; b += align256(sizeof(unsigned) * (size_t)L.nwords);
+    const size_t el = hc_allow_pull(n, flags) ? (size_t)std::max(arcs, 1ll) : 1;  // pull edge list
+    L.bk = b; b += align256(sizeof(unsigned long long) * (kMaxPass + 1));
+    L.psrc = b; b += align256(sizeof(int) * el);
+    L.pdst = b; b += align256(sizeof(int) * el);
+    // edge-list build: bucket-major count matrix over the batch capacity + scan temp
+    L.nbcap = hc_allow_pull(n, flags) ? (n + 31) / 32 + (L.hcap + 31) / 32 : 0;
+    long long ncnt = std::max(1ll, L.npass * L.nbcap);
+    L.elc = b; b += align256(sizeof(unsigned long long) * (size_t)ncnt);
+    L.eltb = 0;
+    cub::DeviceScan::ExclusiveSum((void *)nullptr, L.eltb, (unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, (int)ncnt);
+    L.elt = b; b += align256(L.eltb);
     L.total = b;
     return L;
 }
@@ -1085,9 +1266,11 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.ctl = (Ctrl *)(p + L.ctl);
     a.fsz = (unsigned long long *)(p + L.fsz);
     a.rarcs = (unsigned long long *)(p + L.rarcs);
+    a.rtime = (unsigned long long *)(p + L.rtime);
     a.fsz_cap = kFszCap;
     a.histo = (int *)(p + L.histo);
     a.c8 = (shadow_t *)(p + L.c8);
+    a.rec = (unsigned *)(p + L.rec);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
     a.BC = (int *)(p + L.BC);
@@ -1098,12 +1281,14 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.db = (unsigned char *)(p + L.db);
     a.slen = (int *)(p + L.slen);
     a.capd = (unsigned *)(p + L.capd);
+    a.boff = (unsigned long long *)(p + L.bk);
+    a.psrc = (int *)(p + L.psrc);
+    a.pdst = (int *)(p + L.pdst);
+    a.npass = L.npass;
+    a.pw = (int)std::max(1ll, (n + L.npass - 1) / L.npass);
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)n; a.arcs = arcs; a.core = core; a.tn = tn;
-    // Pull pays when push's remote histogram RMWs and shadow gathers miss L2,
-    // i.e. on graphs whose per-vertex arrays outgrow it (measured: C2 push is
-    // 1.15x faster, RMAT-26 mixed push/pull 1.14x faster than push only).
-    a.allow_pull = (flags & PICO_F_PUSH_ONLY) ? 0 : (flags & PICO_F_PULL_ALWAYS) ? 1 : (n >= kPullMinN);
+    a.allow_pull = hc_allow_pull(n, flags);
     a.nv16 = a.c8;
     a.nv32 = a.oldc;
     a.prefilter = (flags & PICO_F_PREFILTER) ? 1 : 0;
@@ -1148,6 +1333,16 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         int nb = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
         hc_shadow_kernel<<<std::max(nb, 1), 256, 0, s>>>(a);
         launches += 5;
+        if (a.allow_pull && arcs > 0) {  // bucketed edge list for the pull rounds
+            unsigned long long *cnt = (unsigned long long *)(p + L.elc);
+            hc_edgelist_kernel<false><<<sms * 16, 256, 0, s>>>(a, L.nbcap, cnt);
+            size_t tb = L.eltb;
+            if ((err = cub::DeviceScan::ExclusiveSum(p + L.elt, tb, cnt, cnt, (int)(L.npass * L.nbcap), s)))
+                return err;
+            hc_edgelist_kernel<true><<<sms * 16, 256, 0, s>>>(a, L.nbcap, cnt);
+            hc_edgelist_offsets_kernel<<<1, 32, 0, s>>>(a, L.nbcap, cnt);
+            launches += 4;
+        }
     }
     tm.stop();
     if ((err = cudaGetLastError())) return err;
@@ -1207,7 +1402,12 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 return err;
             if ((err = cudaStreamSynchronize(s))) return err;
             size_t nr = (size_t)std::min<unsigned long long>(devrounds + 2, kFszCap);
-            std::vector<unsigned long long> dsz(nr, 0), dar(nr, 0);
+            std::vector<unsigned long long> dsz(nr, 0), dar(nr, 0), dtm(2 * nr + 1, 0);
+            if (st && st->round_ns) {
+                if ((err = cudaMemcpyAsync(dtm.data(), a.rtime, sizeof(unsigned long long) * (2 * nr + 1),
+                                           cudaMemcpyDeviceToHost, s)))
+                    return err;
+            }
             if ((err = cudaMemcpyAsync(dsz.data(), a.fsz, sizeof(unsigned long long) * nr,
                                        cudaMemcpyDeviceToHost, s)))
                 return err;
@@ -1215,6 +1415,14 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                                        cudaMemcpyDeviceToHost, s)))
                 return err;
             if ((err = cudaStreamSynchronize(s))) return err;
+            if (st && st->round_ns) {
+                // phases of rounds 1..devrounds+1 (the last one found F empty)
+                for (unsigned long long t = 1; t <= devrounds + 1 && 2 * t <= 2 * nr; t++) {
+                    if ((int64_t)(2 * t) > 2 * st->frontier_sizes_cap) break;
+                    st->round_ns[2 * (t - 1)] = (int64_t)(dtm[2 * t - 1] - dtm[2 * t - 2]);
+                    st->round_ns[2 * (t - 1) + 1] = (int64_t)(dtm[2 * t] - dtm[2 * t - 1]);
+                }
+            }
             rounds += devrounds;
             for (unsigned long long t = 1; t <= devrounds && t < kFszCap; t++) hsz.push_back(dsz[t]);
             for (unsigned long long t = 1; t <= devrounds + 1 && t < nr; t++) harcs.push_back(dar[t]);
@@ -1455,9 +1663,11 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.ctl = (Ctrl *)(p + L.ctl);
     a.fsz = (unsigned long long *)(p + L.fsz);
     a.rarcs = (unsigned long long *)(p + L.rarcs);
+    a.rtime = (unsigned long long *)(p + L.rtime);
     a.fsz_cap = kFszCap;
     a.histo = (int *)(p + L.histo);
     a.c8 = (shadow_t *)(p + L.c8);
+    a.rec = (unsigned *)(p + L.rec);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
     a.BC = (int *)(p + L.BC);
@@ -1471,6 +1681,10 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)nloc; a.arcs = h->arcs; a.tn = hc_tune(flags);
     a.allow_pull = 0;
+    a.npass = 1;
+    a.pw = (int)std::max(1ll, nloc);
+    a.boff = nullptr;
+    a.psrc = a.pdst = nullptr;
     a.prefilter = 0;  // the shard's UpdateHisto walks the CSC, not the rows
     p += align256(L.total);
     h->deg16g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);

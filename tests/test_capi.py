@@ -66,9 +66,21 @@ def test_host_side_argument_errors(lib):
     assert lib.pico_coreness_host(P, ci.ctypes.data, 0, 0, 0, None, None, 0, None) == 0
 
 
-def test_stats_struct_layout():
-    # pico_stats_t: 16 int64 + double[8] + int64[8] + pointer + int64 + pointer
-    assert ctypes.sizeof(_lib.Stats) == 16 * 8 + 8 * 8 + 8 * 8 + 8 + 8 + 8
+def test_stats_struct_layout(tmp_path):
+    """The ctypes mirror of pico_stats_t matches the C header field by field
+    (offsets and size from gcc on include/pico.h)."""
+    import subprocess
+    from paper_2402_15253_b200.build import INCLUDE
+    fields = [f for f, _ in _lib.Stats._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"pico.h\"\nint main(void){\n"
+                   + "".join(f'printf("%zu\\n", offsetof(pico_stats_t, {f}));\n' for f in fields)
+                   + 'printf("%zu\\n", sizeof(pico_stats_t));return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I" + INCLUDE, str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = [getattr(_lib.Stats, f).offset for f in fields] + [ctypes.sizeof(_lib.Stats)]
+    assert got == want
 
 
 def test_python_api_refuses_cpu_tensors(lib):

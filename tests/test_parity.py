@@ -189,3 +189,32 @@ def test_gpu_generator_matches_cpu():
     c = synth.erdos_renyi(300, 0.05, seed=9, device="cpu")
     d = synth.erdos_renyi(300, 0.05, seed=9, device=torch.device("cuda:0"))
     assert torch.equal(c[1], d[1].cpu())
+
+
+def test_unsorted_rows_pull_passes():
+    """Rows in arbitrary order are allowed (include/pico.h): the pull passes
+    need ascending rows, detect the unsorted input and run a single pass --
+    same coreness and the same |F_t| sequence."""
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    ref = oracle.bz(rp, ci)
+    jac = oracle.jacobi_rounds(rp, ci)
+    rng = np.random.default_rng(7)
+    ci2 = ci.copy()
+    for v in range(rp.size - 1):
+        seg = ci2[rp[v]:rp[v + 1]]
+        rng.shuffle(seg)
+    pico = _pico()
+    for fl in (pico.F_PULL_ALWAYS | pico.F_TINY_TILES, pico.F_PULL_ALWAYS, pico.F_TINY_TILES, 0):
+        _check(rp, ci2, "histocore", fl, ref, jac)
+
+
+def test_c1_pull_always_passes():
+    """C1 with every round in the pull direction, single pass and (tiny
+    tiles) three v-range passes."""
+    rp, ci = synth.to_numpy(*synth.CONFIGS["C1"].build())
+    ref = oracle.bz(rp, ci)
+    jac = oracle.jacobi_rounds(rp, ci)
+    pico = _pico()
+    for fl in (pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
+               pico.F_PULL_ALWAYS | pico.F_TINY_TILES | pico.F_HOST_LOOP):
+        _check(rp, ci, "histocore", fl, ref, jac)
