@@ -114,8 +114,9 @@ enum {
     PICO_K_UPDATE = 4,   /* host-loop mode: UpdateHisto launches            */
     PICO_K_PEEL = 5,     /* P1-P3: PeelOne level loop                        */
     PICO_K_VALIDATE = 6,
-    PICO_K_OTHER = 7,
-    PICO_K_COUNT = 8
+    PICO_K_OTHER = 7,    /* internal compaction of isolated vertex ids       */
+    PICO_K_EDGELIST = 8, /* HistoCore: bucketed edge list of the pull rounds */
+    PICO_K_COUNT = 9
 };
 
 typedef struct {

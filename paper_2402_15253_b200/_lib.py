@@ -25,7 +25,7 @@ F_NO_RELABEL = 512
 F_CLAMP_CAS = 1024
 F_PREFILTER = 2048
 
-K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel"]
+K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel", "edgelist"]
 
 STATUS = {0: "PICO_OK", 1: "PICO_EINVAL", 2: "PICO_ENOTSUP", 3: "PICO_ENOMEM",
           4: "PICO_ECUDA", 5: "PICO_ENCCL", 6: "PICO_EGRAPH"}
@@ -57,8 +57,8 @@ class Stats(ctypes.Structure):
         ("segments_init", ctypes.c_int64),
         ("kernel_count", ctypes.c_int64),
         ("pull_rounds", ctypes.c_int64),
-        ("kernel_ms", ctypes.c_double * 8),
-        ("kernel_launches", ctypes.c_int64 * 8),
+        ("kernel_ms", ctypes.c_double * 9),
+        ("kernel_launches", ctypes.c_int64 * 9),
         ("frontier_sizes", ctypes.POINTER(ctypes.c_int64)),
         ("frontier_sizes_cap", ctypes.c_int64),
         ("round_arcs", ctypes.POINTER(ctypes.c_int64)),
@@ -67,8 +67,8 @@ class Stats(ctypes.Structure):
 
     def to_dict(self) -> dict:
         d = {k: int(getattr(self, k)) for k, _ in self._fields_[:16]}
-        d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(8) if self.kernel_launches[i]}
-        d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(8) if self.kernel_launches[i]}
+        d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(9) if self.kernel_launches[i]}
+        d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(9) if self.kernel_launches[i]}
         return d
 
 

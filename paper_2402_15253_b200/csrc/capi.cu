@@ -103,6 +103,9 @@ static int fail(int code, const char *fmt, ...) {
 static int cuda_fail(cudaError_t e, const char *where) {
     cudaGetLastError();  // clear sticky-free errors
     if (e == cudaErrorMemoryAllocation) return fail(PICO_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
+    if (e == cudaErrorAssert)  // raised by the library itself, not a device assert
+        return fail(PICO_EGRAPH, "%s: histogram invariant violated (input is not a symmetric, deduplicated, "
+                    "loop-free CSR?)", where);
     return fail(PICO_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 

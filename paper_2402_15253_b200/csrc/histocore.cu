@@ -61,21 +61,26 @@ namespace pico {
 #endif
 // vertex count from which dense rounds may run UpdateHisto in the pull direction
 #ifndef PICO_PULL_MIN_N
-#define PICO_PULL_MIN_N (16ll << 20)
+#define PICO_PULL_MIN_N (1ll << 20)
 #endif
 constexpr long long kPullMinN = PICO_PULL_MIN_N;
 // arcs per UpdateHisto work item (segment of a changed row)
 #ifndef PICO_HC_SEG
 #define PICO_HC_SEG 64
 #endif
-typedef unsigned short shadow_t;
-constexpr unsigned SAT8 = 65535;   // degree shadow saturation
+typedef unsigned char shadow_t;
+constexpr unsigned SAT8 = 255;     // degree shadow saturation
 constexpr unsigned RSAT = 65535;   // estimate-record half saturation
 // pull-mode v-range passes: the record slice one pass gathers from
 #ifndef PICO_PASS_MB
 #define PICO_PASS_MB 32
 #endif
 constexpr int kMaxPass = 8;
+// class-C InitHisto shared-memory bins (a vertex whose h-index reaches the
+// cap is redone with global bins; h_1 <= the graph's degree h-index)
+#ifndef PICO_CBINS
+#define PICO_CBINS 16384
+#endif
 #ifndef PICO_PULL_AGG
 #define PICO_PULL_AGG 0            // warp-aggregate duplicate bin moves in pull mode
 #endif                             // (__match_any_sync; measured 1.4-3x slower)
@@ -86,7 +91,8 @@ struct HcArgs {
     int n;
     long long arcs;
     int *core;             // [n]  (core_out)
-    shadow_t *c8;          // [n]  saturated degree shadow (InitHisto)
+    shadow_t *c8;          // [n]  min(deg, 255): degree shadow for rows with deg <= 255
+    unsigned short *c16;   // [n]  min(deg, 65535): degree shadow for longer rows
     unsigned *rec;         // [n]  estimate record (new16 | old16 << 16)
     int *oldc;             // [n]
     int *histo;            // [2m]
@@ -104,7 +110,8 @@ struct HcArgs {
     Ctrl *ctl;
     Tune tn;
     int allow_pull;
-    const shadow_t *nv16;  // neighbour-degree lookups of InitHisto (see init_val)
+    const shadow_t *nv8;   // neighbour-degree lookups of InitHisto (see init_val)
+    const unsigned short *nv16;
     const int *nv32;
     // degree prefilter (push UpdateHisto): rows copied in descending order of
     // the neighbours' degree bucket floor(log2 deg); a changed v with new
@@ -118,7 +125,7 @@ struct HcArgs {
     // of the neighbour, bucket p = {v in [p*pw, (p+1)*pw)} at
     // [boff[p], boff[p+1]) of psrc (= u) / pdst (= v); a pass over one
     // bucket gathers the records of an L2-sized slice of the vertices
-    int npass, pw;
+    int npass, pshift;
     unsigned long long *boff;  // [kMaxPass + 1] bucket offsets
     int *psrc, *pdst;
 };
@@ -143,7 +150,7 @@ __device__ __forceinline__ int scan_len(const HcArgs &a, long long hb, int d, in
 __device__ __forceinline__ int nseg_of(long long d, int seg) { return (int)((d + seg - 1) / seg); }
 
 // 16-bit load (hot policy)
-__device__ __forceinline__ unsigned ld_shadow(const unsigned short *p, unsigned long long hot) {
+__device__ __forceinline__ unsigned ld_shadow(const unsigned char *p, unsigned long long hot) {
 #if PICO_L2_HINTS
     return ld_cg_u16(p, hot);
 #else
@@ -171,6 +178,7 @@ __device__ __forceinline__ int core_of(const HcArgs &a, int u, unsigned long lon
 
 __device__ __forceinline__ void set_c8(const HcArgs &a, int v, int k) {
     a.c8[v] = (shadow_t)min(k, (int)SAT8);
+    a.c16[v] = (unsigned short)min(k, 65535);
 }
 
 // warp-aggregated reservation of nseg segments per lane; writes (v, s) entries
@@ -319,12 +327,21 @@ __global__ void __launch_bounds__(512) hc_reorder_cta_kernel(HcArgs a) {
 }
 
 // neighbour degree for init, clamped to d (the histogram cap of P:498)
-// (nv16 / nv32: degree of every neighbour id -- the local shadow / oldcore on
-// one GPU, the all-gathered global degrees on a shard)
+// (nv8 / nv16 / nv32: degree of every neighbour id saturated at 255, at
+// 65535, and exact; the local shadows / oldcore on one GPU, the all-gathered
+// global degrees on a shard).  The thread-per-vertex class (d <= 16) gathers
+// the 1-byte shadow, exact for it and half the L2 footprint (measured: 1.2x
+// faster at RMAT-26); the warp and CTA classes gather the 2-byte one (a
+// 1-byte shadow plus exact fallback was measured 1.1-1.7x slower for them:
+// their neighbours are often hubs).
+__device__ __forceinline__ int init_val_small(const HcArgs &a, int u, int d, unsigned long long hot) {
+    return min((int)ld_shadow(a.nv8 + u, hot), d);  // d <= 16 < 255: exact
+}
+
 __device__ __forceinline__ int init_val(const HcArgs &a, int u, int d, unsigned long long hot) {
-    int x = (int)ld_shadow(a.nv16 + u, hot);
+    int x = (int)__ldcg(a.nv16 + u);
     if (x >= d) return d;
-    if (x == (int)SAT8) return min(__ldg(a.nv32 + u), d);
+    if (x == 65535) return min(__ldg(a.nv32 + u), d);
     return x;
 }
 
@@ -358,7 +375,7 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
             for (int e = 0; e < d; e++) {
                 int u = ld_stream(a.ci + hb + e, cold);
                 if (a.prefilter) a.ro[hb + e] = u;  // short rows: copied in order
-                int x = init_val(a, u, d, hot);     // min(core[u], core[v])
+                int x = init_val_small(a, u, d, hot);  // min(core[u], core[v])
 #pragma unroll
                 for (int b = 0; b < NB; b++) cnt[b] += (x == b + 1);
             }
@@ -410,7 +427,20 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         int d = (int)(a.rp[v + 1] - hb);
         for (int b = lane; b <= d; b += 32) bins[b] = 0;
         __syncwarp();
-        for (int e = lane; e < d; e += 32) atomicAdd(&bins[init_val(a, ld_stream(a.ci + hb + e, cold), d, hot)], 1);
+        {
+            int e = lane;
+            for (; e + 96 < d; e += 128) {  // 4 gathers in flight per lane
+                int u0 = ld_stream(a.ci + hb + e, cold), u1 = ld_stream(a.ci + hb + e + 32, cold);
+                int u2 = ld_stream(a.ci + hb + e + 64, cold), u3 = ld_stream(a.ci + hb + e + 96, cold);
+                int x0 = init_val(a, u0, d, hot), x1 = init_val(a, u1, d, hot);
+                int x2 = init_val(a, u2, d, hot), x3 = init_val(a, u3, d, hot);
+                atomicAdd(&bins[x0], 1);
+                atomicAdd(&bins[x1], 1);
+                atomicAdd(&bins[x2], 1);
+                atomicAdd(&bins[x3], 1);
+            }
+            for (; e < d; e += 32) atomicAdd(&bins[init_val(a, ld_stream(a.ci + hb + e, cold), d, hot)], 1);
+        }
         __syncwarp();
         // descending walk for the h-index (SumHisto on the fresh histogram)
         int carry = 0, top = d, h = 0, hs = 0;
@@ -472,8 +502,20 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
         if (!GLOBAL || b >= 1) bins[b] = 0;
     __syncthreads();
     const unsigned long long hot = pol_last(), cold = pol_first();
-    for (int e = tid; e < d; e += nt)
-        atomicAdd(&bins[min(init_val(a, ld_stream(a.ci + hb + e, cold), d, hot), B)], 1);
+    {
+        int e = tid;
+        for (; e + 3 * nt < d; e += 4 * nt) {  // 4 gathers in flight per thread
+            int u0 = ld_stream(a.ci + hb + e, cold), u1 = ld_stream(a.ci + hb + e + nt, cold);
+            int u2 = ld_stream(a.ci + hb + e + 2 * nt, cold), u3 = ld_stream(a.ci + hb + e + 3 * nt, cold);
+            int x0 = init_val(a, u0, d, hot), x1 = init_val(a, u1, d, hot);
+            int x2 = init_val(a, u2, d, hot), x3 = init_val(a, u3, d, hot);
+            atomicAdd(&bins[min(x0, B)], 1);
+            atomicAdd(&bins[min(x1, B)], 1);
+            atomicAdd(&bins[min(x2, B)], 1);
+            atomicAdd(&bins[min(x3, B)], 1);
+        }
+        for (; e < d; e += nt) atomicAdd(&bins[min(init_val(a, ld_stream(a.ci + hb + e, cold), d, hot), B)], 1);
+    }
     __syncthreads();
     // block-wide descending search: h = max b in 1..B with sum_{j>=b} bins[j] >= b
     int c = (B + nt - 1) / nt;
@@ -579,93 +621,115 @@ __global__ void hc_shadow_kernel(HcArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Edge list of the pull rounds, bucketed by the neighbour's v-range, in CSR
-// order inside each bucket: work batches (32 short rows, then 32 static hub
-// segments) count their arcs per bucket, one exclusive scan over the
-// bucket-major count matrix gives every (bucket, batch) its output offset,
-// and the batches write their (u, v) pairs in row order.
+// Edge list of the pull rounds, bucketed by the neighbour's v-range
+// (bucket p = v >> pshift), in CSR order inside each bucket:
+//   src:   the row owning every arc (short rows one thread each, hub rows a
+//          warp per static 64-arc segment)
+//   count: per 2048-arc chunk and bucket (ballot/popc), bucket-major matrix
+//   scan:  one exclusive scan -> every (bucket, chunk) output offset
+//   fill:  each chunk writes its (u, v) pairs in arc order
+// With one bucket the edge list is (src, colidx) itself: no count/fill.
 // ---------------------------------------------------------------------------
-// lane's arc range of edge-list batch bidx (short rows, then hub segments)
-__device__ __forceinline__ void el_batch(const HcArgs &a, long long bidx, long long nvb, long long nh, int &uu,
-                                         long long &b, int &len) {
+constexpr int kElChunk = 2048;
+
+// rows of the thread-per-vertex class (deg <= a_max): one thread each
+__global__ void hc_el_src_short_kernel(HcArgs a, int *src) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < a.n; u += nthreads) {
+        long long r0 = a.rp[u], r1 = a.rp[u + 1];
+        if (r1 - r0 <= a.tn.a_max)
+            for (long long e = r0; e < r1; e++) src[e] = (int)u;
+    }
+}
+
+// longer rows (the degree-class lists B and C): one warp per row, coalesced
+__global__ void hc_el_src_long_kernel(HcArgs a, int *src) {
+    const long long nB = (long long)bcast_u64(&a.ctl->nB), nC = (long long)bcast_u64(&a.ctl->nC);
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = gw; i < nB + nC; i += nw) {
+        const int u = i < nB ? a.BC[i] : a.BC[a.n - 1 - (i - nB)];
+        const long long r0 = a.rp[u], r1 = a.rp[u + 1];
+        for (long long x = r0 + lane_id(); x < r1; x += 32) src[x] = u;
+    }
+}
+
+// warp per chunk: counts[p * nchunk + c] (per-lane counters, 8 loads in
+// flight per lane, one warp reduction per bucket at the end of the chunk)
+__global__ void __launch_bounds__(256) hc_el_count_kernel(HcArgs a, unsigned long long *cnt, long long nchunk) {
     const int lane = lane_id();
-    uu = 0; b = 0; len = 0;
-    if (bidx < nvb) {
-        long long v = bidx * 32 + lane;
-        if (v < a.n) {
-            long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-            if (r1 - r0 <= a.tn.seg) { uu = (int)v; b = r0; len = (int)(r1 - r0); }
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long cold = pol_first();
+    for (long long c = gw; c < nchunk; c += nw) {
+        const long long e0 = c * kElChunk, e1 = min(e0 + kElChunk, a.arcs);
+        int k[kMaxPass] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (long long eb = e0; eb < e1; eb += 8 * 32) {
+            int v[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                long long e = eb + i * 32 + lane;
+                v[i] = e < e1 ? ld_stream(a.ci + e, cold) >> a.pshift : -1;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int q = 0; q < kMaxPass; q++) k[q] += (v[i] == q);
         }
-    } else {
-        long long i = (bidx - nvb) * 32 + lane;
-        if (i < nh) {
-            int2 sg = a.H[i];
-            long long r0 = __ldg(a.rp + sg.x), r1 = __ldg(a.rp + sg.x + 1);
-            uu = sg.x;
-            b = r0 + (long long)sg.y * a.tn.seg;
-            len = (int)min((long long)a.tn.seg, r1 - b);
+#pragma unroll
+        for (int q = 0; q < kMaxPass; q++) {
+            if (q >= a.npass) break;
+            long long t = warp_sum64(k[q]);
+            if (lane == 0) cnt[(long long)q * nchunk + c] = (unsigned long long)t;
         }
     }
 }
 
-template <bool FILL>
-__global__ void __launch_bounds__(256) hc_edgelist_kernel(HcArgs a, long long nbcap, unsigned long long *cnt) {
+// warp per chunk: the scanned counts are the output offsets; 4 steps of 32
+// arcs in flight, one ballot per bucket and step
+__global__ void __launch_bounds__(256) hc_el_fill_kernel(HcArgs a, const int *src, const unsigned long long *off,
+                                                         long long nchunk) {
     const int lane = lane_id();
     const unsigned lt = (1u << lane) - 1;
-    const long long nvb = ((long long)a.n + 31) >> 5;
-    const long long nh = (long long)bcast_u64(&a.ctl->nH);
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long bidx = gw; bidx < nbcap; bidx += nw) {
-        int uu, len;
-        long long b;
-        el_batch(a, bidx, nvb, nh, uu, b, len);
-        int incl = warp_incl_scan(len);
-        int excl = incl - len;
-        int total = __shfl_sync(FULL, incl, 31);
+    const unsigned long long cold = pol_first();
+    for (long long c = gw; c < nchunk; c += nw) {
+        const long long e0 = c * kElChunk, e1 = min(e0 + kElChunk, a.arcs);
         unsigned long long cur[kMaxPass];
 #pragma unroll
-        for (int q = 0; q < kMaxPass; q++) cur[q] = FILL && q < a.npass ? cnt[(long long)q * nbcap + bidx] : 0;
-        for (int j0 = 0; j0 < total; j0 += 32) {
-            int j = j0 + lane;
-            int lo = 0;
+        for (int q = 0; q < kMaxPass; q++) cur[q] = q < a.npass ? off[(long long)q * nchunk + c] : 0;
+        for (long long eb = e0; eb < e1; eb += 4 * 32) {
+            int v[4], u[4];
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                int cand = lo + step;
-                int ex = __shfl_sync(FULL, excl, cand & 31);
-                if (cand < 32 && ex <= j) lo = cand;
+            for (int i = 0; i < 4; i++) {
+                long long e = eb + i * 32 + lane;
+                v[i] = e < e1 ? ld_stream(a.ci + e, cold) : -1;
+                u[i] = e < e1 ? ld_stream(src + e, cold) : 0;
             }
-            long long eb = __shfl_sync(FULL, b, lo);
-            int ex = __shfl_sync(FULL, excl, lo);
-            int uo = __shfl_sync(FULL, uu, lo);
-            int v = j < total ? __ldg(a.ci + eb + (j - ex)) : 0;
-            int p = j < total ? v / a.pw : -1;
 #pragma unroll
-            for (int q = 0; q < kMaxPass; q++) {
-                if (q >= a.npass) break;
-                unsigned m = __ballot_sync(FULL, p == q);
-                if (FILL && p == q) {
-                    unsigned long long w = cur[q] + __popc(m & lt);
-                    a.psrc[w] = uo;
-                    a.pdst[w] = v;
+            for (int i = 0; i < 4; i++) {
+                const int p = v[i] >= 0 ? v[i] >> a.pshift : -1;
+#pragma unroll
+                for (int q = 0; q < kMaxPass; q++) {
+                    if (q >= a.npass) break;
+                    const unsigned m = __ballot_sync(FULL, p == q);
+                    if (p == q) {
+                        const unsigned long long w = cur[q] + __popc(m & lt);
+                        a.psrc[w] = u[i];
+                        a.pdst[w] = v[i];
+                    }
+                    cur[q] += __popc(m);
                 }
-                cur[q] += __popc(m);
             }
-        }
-        if (!FILL && lane < a.npass) {
-            unsigned long long c = 0;
-#pragma unroll
-            for (int q = 0; q < kMaxPass; q++)
-                if (q == lane) c = cur[q];
-            cnt[(long long)lane * nbcap + bidx] = c;
         }
     }
 }
 
 // bucket offsets from the scanned count matrix
-__global__ void hc_edgelist_offsets_kernel(HcArgs a, long long nbcap, const unsigned long long *off) {
+__global__ void hc_el_offsets_kernel(HcArgs a, long long nchunk, const unsigned long long *off) {
     if (threadIdx.x <= kMaxPass)
-        a.boff[threadIdx.x] = (int)threadIdx.x < a.npass ? off[(long long)threadIdx.x * nbcap] : (unsigned long long)a.arcs;
+        a.boff[threadIdx.x] = (int)threadIdx.x < a.npass ? off[(long long)threadIdx.x * nchunk] : (unsigned long long)a.arcs;
 }
 
 // ---------------------------------------------------------------------------
@@ -851,9 +915,12 @@ __device__ void update_phase(const HcArgs &a, int t) {
 // random access per arc is the 4-byte record of v, inside the bucket's
 // L2-sized vertex slice.  No owner search, no per-row bookkeeping.
 // ---------------------------------------------------------------------------
+#ifndef PICO_PULL_U
+#define PICO_PULL_U 4
+#endif
 template <bool STATS>
 __device__ void coo_pull_phase(const HcArgs &a, int t) {
-    constexpr int UA = PICO_ARC_U;
+    constexpr int UA = PICO_PULL_U;
     const int lane = lane_id();
     const unsigned *chg = a.chg + (t & 1) * a.nwords;
     long long st_arcs = 0, st_guard = 0;
@@ -905,9 +972,9 @@ __device__ void coo_pull_phase(const HcArgs &a, int t) {
             }
             bool g = ok && ch && cv < cu;  // N1/N3 neighbour
             if (STATS) st_guard += g;
+            // source bin min(oldcore[v], core[u]): the cap bin iff oldcore[v] >= core[u]
+            const bool capdec = ov >= cu;
             if (g) {
-                // source bin min(oldcore[v], core[u]): the cap bin iff oldcore[v] >= core[u]
-                const bool capdec = ov >= cu;
                 red_add(a.histo + hb[q] + (capdec ? cu : ov), -1);
                 if (capdec) red_or(a.capd + (u[q] >> 5), 1u << (u[q] & 31));
                 red_add(a.histo + hb[q] + cv, 1);
@@ -941,6 +1008,8 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
         d = __ldg(a.rp + v + 1) - hb - 1;
         k = cold;
         done = false;
+        // (a broken invariant can walk k below 1 here: the warp loop below
+        // then stops at once)
         for (int stp = 0; stp < 32; stp++) {
             sum += __ldcg(a.histo + hb + k);
             if (STATS) st_bins++;
@@ -967,6 +1036,15 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
                 int f = __ffs(mm) - 1;
                 rk = kL - f;
                 rs = __shfl_sync(FULL, s, f);
+                break;
+            }
+            if (kL <= 32) {
+                // no bin down to 1 reaches its index: a histogram invariant
+                // is broken (the input is not a symmetric deduplicated
+                // loop-free CSR); stop instead of walking on forever
+                if (lane == 0) *reinterpret_cast<volatile int *>(&a.ctl->error) = 1;
+                rk = 1;
+                rs = 1;
                 break;
             }
             sL += __shfl_sync(FULL, incl, 31);
@@ -1100,6 +1178,10 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
         if (leader && (unsigned long long)t < a.fsz_cap) a.rtime[2 * t] = globaltimer();
         unsigned long long nf = bcast_u64(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
+        if ((unsigned long long)t + 1 >= a.fsz_cap) {  // far beyond any valid l2: broken input
+            if (leader) *reinterpret_cast<volatile int *>(&a.ctl->error) = 1;
+            break;
+        }
         if (leader) {
             a.ctl->rounds++;
             if ((unsigned long long)t < a.fsz_cap) a.fsz[t] = nf;
@@ -1147,10 +1229,10 @@ Tune hc_tune(uint32_t flags) {
     if (flags & PICO_F_TINY_TILES) {
         t.a_max = 4; t.b_max = 12; t.c_bins = 16; t.seg = 4;
     } else {
-        t.a_max = 16; t.b_max = 1024; t.c_bins = 40960; t.seg = PICO_HC_SEG;
+        t.a_max = 16; t.b_max = 1024; t.c_bins = PICO_CBINS; t.seg = PICO_HC_SEG;
     }
 #ifndef PICO_PULL_DIV
-#define PICO_PULL_DIV 8
+#define PICO_PULL_DIV 2
 #endif
     t.pull_div = PICO_PULL_DIV;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
     if (flags & PICO_F_PULL_ALWAYS) t.pull_div = 1 << 30;
@@ -1162,16 +1244,26 @@ static bool hc_allow_pull(long long n, uint32_t flags) {
     return (flags & PICO_F_PUSH_ONLY) ? false : (flags & PICO_F_PULL_ALWAYS) ? true : (n >= kPullMinN);
 }
 
+// v-range width of a pull pass: 2^shift vertices whose 4-byte records fit
+// PICO_PASS_MB (the L2 slice one pass gathers from), at most kMaxPass passes
+static int hc_pshift(long long n, uint32_t flags) {
+    int sh = 0;
+    if (flags & PICO_F_TINY_TILES) {  // exercise the passes on small graphs
+        while ((1ll << sh) * 3 < n) sh++;
+    } else {
+        while ((4ll << (sh + 1)) <= ((long long)PICO_PASS_MB << 20)) sh++;
+    }
+    while (((n - 1) >> sh) + 1 > kMaxPass) sh++;
+    return sh;
+}
+
 static int hc_npass(long long n, uint32_t flags) {
     if (!hc_allow_pull(n, flags) || n < 2) return 1;
-    if (flags & PICO_F_TINY_TILES) return (int)std::min<long long>(3, n);  // exercise the passes
-    long long per = (long long)PICO_PASS_MB << 20;
-    long long np = (4 * n + per - 1) / per;  // 4-byte records per pass <= PICO_PASS_MB
-    return (int)std::max(1ll, std::min<long long>(np, kMaxPass));
+    return (int)(((n - 1) >> hc_pshift(n, flags)) + 1);
 }
 
 struct HcLayout {
-    size_t ctl, fsz, rarcs, rtime, histo, c8, rec, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
+    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
         elc, elt, total;
     long long nwords, scap, hcap, nbcap;
     size_t eltb;
@@ -1192,6 +1284,7 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     L.rtime = b; b += align256(sizeof(unsigned long long) * (2 * kFszCap + 1));
     L.histo = b; b += align256(sizeof(int) * (size_t)arcs);
     L.c8 = b; b += align256(sizeof(shadow_t) * (size_t)n);
+    L.c16 = b; b += align256(sizeof(unsigned short) * (size_t)n);
     L.rec = b; b += align256(sizeof(unsigned) * (size_t)n);
     L.oldc = b; b += align256(sizeof(int) * (size_t)n);
     L.F = b; b += align256(sizeof(int) * (size_t)n);
@@ -1206,9 +1299,9 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     const size_t el = hc_allow_pull(n, flags) ? (size_t)std::max(arcs, 1ll) : 1;  // pull edge list
     L.bk = b; b += align256(sizeof(unsigned long long) * (kMaxPass + 1));
     L.psrc = b; b += align256(sizeof(int) * el);
-    L.pdst = b; b += align256(sizeof(int) * el);
-    // edge-list build: bucket-major count matrix over the batch capacity + scan temp
-    L.nbcap = hc_allow_pull(n, flags) ? (n + 31) / 32 + (L.hcap + 31) / 32 : 0;
+    L.pdst = b; b += align256(sizeof(int) * (L.npass > 1 ? el : 1));  // one bucket: colidx itself
+    // edge-list build: bucket-major count matrix over the 2048-arc chunks + scan temp
+    L.nbcap = (hc_allow_pull(n, flags) && L.npass > 1) ? (arcs + kElChunk - 1) / kElChunk : 0;
     long long ncnt = std::max(1ll, L.npass * L.nbcap);
     L.elc = b; b += align256(sizeof(unsigned long long) * (size_t)ncnt);
     L.eltb = 0;
@@ -1270,6 +1363,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.fsz_cap = kFszCap;
     a.histo = (int *)(p + L.histo);
     a.c8 = (shadow_t *)(p + L.c8);
+    a.c16 = (unsigned short *)(p + L.c16);
     a.rec = (unsigned *)(p + L.rec);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
@@ -1285,11 +1379,13 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.psrc = (int *)(p + L.psrc);
     a.pdst = (int *)(p + L.pdst);
     a.npass = L.npass;
-    a.pw = (int)std::max(1ll, (n + L.npass - 1) / L.npass);
+    a.pshift = hc_pshift(n, flags);
+    if (L.npass == 1) a.pdst = const_cast<int *>(ci);  // one bucket: (src, colidx)
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)n; a.arcs = arcs; a.core = core; a.tn = tn;
     a.allow_pull = hc_allow_pull(n, flags);
-    a.nv16 = a.c8;
+    a.nv8 = a.c8;
+    a.nv16 = a.c16;
     a.nv32 = a.oldc;
     a.prefilter = (flags & PICO_F_PREFILTER) ? 1 : 0;
 
@@ -1311,6 +1407,35 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         launches++;
     }
     tm.stop();
+    // the bucketed edge list is built before InitHisto: it borrows the
+    // histogram space for its row-owner column
+    {
+        if (a.allow_pull && arcs > 0) {  // bucketed edge list for the pull rounds
+            tm.start(PICO_K_EDGELIST);
+            // src goes straight into psrc (one bucket) or through the histogram
+            // space, which InitHisto has not written yet -- see the launch order
+            int *src = L.npass > 1 ? a.histo : a.psrc;
+            int nb = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
+            hc_el_src_short_kernel<<<std::max(nb, 1), 256, 0, s>>>(a, src);
+            hc_el_src_long_kernel<<<sms * 8, 256, 0, s>>>(a, src);
+            launches += 2;
+            if (L.npass > 1) {
+                unsigned long long *cnt = (unsigned long long *)(p + L.elc);
+                hc_el_count_kernel<<<sms * 16, 256, 0, s>>>(a, cnt, L.nbcap);
+                size_t tb = L.eltb;
+                if ((err = cub::DeviceScan::ExclusiveSum(p + L.elt, tb, cnt, cnt, (int)(L.npass * L.nbcap), s)))
+                    return err;
+                hc_el_fill_kernel<<<sms * 16, 256, 0, s>>>(a, src, cnt, L.nbcap);
+                hc_el_offsets_kernel<<<1, 32, 0, s>>>(a, L.nbcap, cnt);
+                launches += 3;
+            } else {
+                unsigned long long off[kMaxPass + 1];
+                for (int q = 0; q <= kMaxPass; q++) off[q] = q == 0 ? 0 : (unsigned long long)arcs;
+                if ((err = cudaMemcpyAsync(a.boff, off, sizeof(off), cudaMemcpyHostToDevice, s))) return err;
+            }
+            tm.stop();
+        }
+    }
     // H1-H3 (round 1)
     tm.start(PICO_K_INIT);
     {
@@ -1324,25 +1449,18 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
         cudaFuncSetAttribute(hc_init_warp_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smB);
-        hc_init_warp_kernel<STATS><<<sms * 4, 256, smB, s>>>(a);
+        int occB = 0, occC = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS>, 256, smB);
+        hc_init_warp_kernel<STATS><<<sms * std::max(1, occB), 256, smB, s>>>(a);
         size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
         cudaFuncSetAttribute(hc_init_cta_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smC);
-        hc_init_cta_kernel<STATS><<<sms, 512, smC, s>>>(a);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, hc_init_cta_kernel<STATS>, 512, smC);
+        hc_init_cta_kernel<STATS><<<sms * std::max(1, occC), 512, smC, s>>>(a);
         hc_init_fallback_kernel<STATS><<<sms, 512, 0, s>>>(a);
         int nb = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
         hc_shadow_kernel<<<std::max(nb, 1), 256, 0, s>>>(a);
         launches += 5;
-        if (a.allow_pull && arcs > 0) {  // bucketed edge list for the pull rounds
-            unsigned long long *cnt = (unsigned long long *)(p + L.elc);
-            hc_edgelist_kernel<false><<<sms * 16, 256, 0, s>>>(a, L.nbcap, cnt);
-            size_t tb = L.eltb;
-            if ((err = cub::DeviceScan::ExclusiveSum(p + L.elt, tb, cnt, cnt, (int)(L.npass * L.nbcap), s)))
-                return err;
-            hc_edgelist_kernel<true><<<sms * 16, 256, 0, s>>>(a, L.nbcap, cnt);
-            hc_edgelist_offsets_kernel<<<1, 32, 0, s>>>(a, L.nbcap, cnt);
-            launches += 4;
-        }
     }
     tm.stop();
     if ((err = cudaGetLastError())) return err;
@@ -1384,7 +1502,12 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 if (nf == 0) break;
                 rounds++;
                 hsz.push_back(nf);
+                if ((unsigned long long)t + 1 >= kFszCap) return cudaErrorAssert;  // broken input
             }
+            int derr = 0;
+            if ((err = cudaMemcpyAsync(&derr, &a.ctl->error, sizeof(derr), cudaMemcpyDeviceToHost, s))) return err;
+            if ((err = cudaStreamSynchronize(s))) return err;
+            if (derr) return cudaErrorAssert;
         } else {
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hc_rounds_kernel<STATS>, 512, 0);
@@ -1397,10 +1520,13 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
             launches++;
             if (err) return err;
             unsigned long long devrounds = 0;
+            int derr = 0;
             if ((err = cudaMemcpyAsync(&devrounds, &a.ctl->rounds, sizeof(devrounds),
                                        cudaMemcpyDeviceToHost, s)))
                 return err;
+            if ((err = cudaMemcpyAsync(&derr, &a.ctl->error, sizeof(derr), cudaMemcpyDeviceToHost, s))) return err;
             if ((err = cudaStreamSynchronize(s))) return err;
+            if (derr) return cudaErrorAssert;  // broken histogram invariant (capi: PICO_EGRAPH)
             size_t nr = (size_t)std::min<unsigned long long>(devrounds + 2, kFszCap);
             std::vector<unsigned long long> dsz(nr, 0), dar(nr, 0), dtm(2 * nr + 1, 0);
             if (st && st->round_ns) {
@@ -1486,7 +1612,8 @@ struct Shard {
     uint32_t flags;
     cudaStream_t s;
     DevInfo dev;
-    shadow_t *deg16g;        // [ng]   saturated global degrees (init)
+    shadow_t *deg8g;         // [ng]   saturated global degrees (init)
+    unsigned short *deg16g;  // [ng]
     long long *csc_off;      // [ng+1]
     long long *csc_cur;      // [ng]
     int *csc_idx;            // [arcs] owned neighbour (local id)
@@ -1498,10 +1625,10 @@ struct Shard {
     int t;
 };
 
-__global__ void sh_deg16_kernel(const int *deg, long long ng, shadow_t *d16) {
+__global__ void sh_deg8_kernel(const int *deg, long long ng, shadow_t *d8, unsigned short *d16) {
     long long nt = (long long)gridDim.x * blockDim.x;
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < ng; v += nt)
-        d16[v] = (shadow_t)min(deg[v], (int)SAT8);
+        d8[v] = (shadow_t)min(deg[v], (int)SAT8), d16[v] = (unsigned short)min(deg[v], 65535);
 }
 
 // CSC counts per global vertex (into csc_off[v+1]) and scatter
@@ -1635,6 +1762,7 @@ size_t shard_workspace_bytes(long long nloc, long long ng, long long arcs, uint3
     Tune tn = hc_tune(flags);
     size_t b = align256(hc_layout(nloc, arcs, flags).total);
     b += align256(sizeof(shadow_t) * (size_t)ng);
+    b += align256(sizeof(unsigned short) * (size_t)ng);
     b += align256(sizeof(long long) * (size_t)(ng + 1)) * 2;
     b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
     *tscap = ng + arcs / tn.seg + 64;
@@ -1667,6 +1795,7 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.fsz_cap = kFszCap;
     a.histo = (int *)(p + L.histo);
     a.c8 = (shadow_t *)(p + L.c8);
+    a.c16 = (unsigned short *)(p + L.c16);
     a.rec = (unsigned *)(p + L.rec);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
@@ -1682,12 +1811,13 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.rp = rp; a.ci = ci; a.n = (int)nloc; a.arcs = h->arcs; a.tn = hc_tune(flags);
     a.allow_pull = 0;
     a.npass = 1;
-    a.pw = (int)std::max(1ll, nloc);
+    a.pshift = 30;
     a.boff = nullptr;
     a.psrc = a.pdst = nullptr;
     a.prefilter = 0;  // the shard's UpdateHisto walks the CSC, not the rows
     p += align256(L.total);
-    h->deg16g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
+    h->deg8g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
+    h->deg16g = (unsigned short *)p; p += align256(sizeof(unsigned short) * (size_t)ng);
     h->csc_off = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
     h->csc_cur = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
     h->csc_idx = (int *)p; p += align256(sizeof(int) * (size_t)std::max(h->arcs, 1ll));
@@ -1729,7 +1859,8 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         return std::max(1, (int)std::min<long long>((work + 255) / 256, (long long)sms * 16));
     };
     cudaError_t e;
-    sh_deg16_kernel<<<grid(h->ng), 256, 0, s>>>(deg_global, h->ng, h->deg16g);
+    sh_deg8_kernel<<<grid(h->ng), 256, 0, s>>>(deg_global, h->ng, h->deg8g, h->deg16g);
+    a.nv8 = h->deg8g;
     a.nv16 = h->deg16g;
     a.nv32 = deg_global;
     // CSC: counts -> exclusive scan -> scatter
@@ -1747,14 +1878,18 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         hc_init_small_kernel<false><<<grid(h->nloc), 256, 0, s>>>(a);
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
         cudaFuncSetAttribute(hc_init_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
-        hc_init_warp_kernel<false><<<sms * 4, 256, smB, s>>>(a);
+        int occB = 0, occC = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false>, 256, smB);
+        hc_init_warp_kernel<false><<<sms * std::max(1, occB), 256, smB, s>>>(a);
         size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
         cudaFuncSetAttribute(hc_init_cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC);
-        hc_init_cta_kernel<false><<<sms, 512, smC, s>>>(a);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, hc_init_cta_kernel<false>, 512, smC);
+        hc_init_cta_kernel<false><<<sms * std::max(1, occC), 512, smC, s>>>(a);
         hc_init_fallback_kernel<false><<<sms, 512, 0, s>>>(a);
         hc_shadow_kernel<<<grid(h->nloc), 256, 0, s>>>(a);
     }
-    a.nv16 = a.c8;
+    a.nv8 = a.c8;
+    a.nv16 = a.c16;
     a.nv32 = a.oldc;
     unsigned long long c1 = 0;
     if ((e = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return e;

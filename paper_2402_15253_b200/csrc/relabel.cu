@@ -7,13 +7,12 @@
 // graph and mapping the result back is bit-exact.
 //
 // Why: on graphs like RMAT-26 half of the 2^26 ids are isolated; dropping them
-// halves every per-vertex array, so the 16-bit estimate shadow (2 B/vertex)
-// and the changed bitmap fit in the 126 MB L2 and the per-arc neighbour
-// gathers stop missing to HBM.  Because isolated rows are empty, arc positions
-// do not move: rowptr2[new(v)] = rowptr[v] and colidx2[e] = new(colidx[e]) is
-// a pure streaming map.  new(u) is computed from two L2-resident arrays (the
-// n-bit non-isolated bitmap and one prefix count per 32-bit word) instead of
-// an n-entry permutation gather.
+// halves every per-vertex array, so more of the per-arc neighbour gathers hit
+// the 126 MB L2.  Because isolated rows are empty, arc positions do not move:
+// rowptr2[new(v)] = rowptr[v] and colidx2[e] = new(colidx[e]) is a pure
+// streaming map.  new(u) comes from one L2-resident 8-byte word per 32 ids
+// (the non-isolated bitmap word and the exclusive prefix count of its
+// predecessors) instead of an n-entry permutation gather.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -44,6 +43,18 @@ __device__ __forceinline__ int rl_rank(const unsigned *bits, const unsigned *wpr
     return (int)(ld_cg_u32(wpre + (u >> 5), hot) + __popc(w & ((1u << (u & 31)) - 1)));
 }
 
+// (bitmap word, prefix) packed: one 8-byte gather per rank
+__global__ void rl_pack_kernel(const unsigned *bits, const unsigned *wpre, long long nwords, uint2 *bw) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += nthreads)
+        bw[w] = make_uint2(bits[w], wpre[w]);
+}
+
+__device__ __forceinline__ int rl_rank2(const uint2 *bw, int u) {
+    uint2 x = __ldcg(bw + (u >> 5));
+    return (int)(x.y + __popc(x.x & ((1u << (u & 31)) - 1)));
+}
+
 // rowptr2 and inverse map
 __global__ void rl_rows_kernel(const long long *rp, long long n, const unsigned *bits, const unsigned *wpre,
                                long long *rp2, int *inv, long long arcs) {
@@ -63,13 +74,22 @@ __global__ void rl_rows_kernel(const long long *rp, long long n, const unsigned 
     }
 }
 
-// colidx2[e] = new(colidx[e]): coalesced stream in, coalesced stream out
-__global__ void rl_arcs_kernel(const int *ci, long long arcs, const unsigned *bits, const unsigned *wpre,
-                               int *ci2) {
-    long long nthreads = (long long)gridDim.x * blockDim.x;
-    const unsigned long long hot = pol_last(), cold = pol_first();
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < arcs; e += nthreads)
-        ci2[e] = rl_rank(bits, wpre, ld_stream(ci + e, cold), hot);
+// colidx2[e] = new(colidx[e]): coalesced stream in, coalesced stream out,
+// four arcs (and their rank gathers) in flight per thread
+__global__ void rl_arcs_kernel(const int *ci, long long arcs, const uint2 *bw, int *ci2) {
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    const unsigned long long cold = pol_first();
+    long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; e + 3 * nthreads < arcs; e += 4 * nthreads) {
+        int u0 = ld_stream(ci + e, cold), u1 = ld_stream(ci + e + nthreads, cold);
+        int u2 = ld_stream(ci + e + 2 * nthreads, cold), u3 = ld_stream(ci + e + 3 * nthreads, cold);
+        int r0 = rl_rank2(bw, u0), r1 = rl_rank2(bw, u1), r2 = rl_rank2(bw, u2), r3 = rl_rank2(bw, u3);
+        ci2[e] = r0;
+        ci2[e + nthreads] = r1;
+        ci2[e + 2 * nthreads] = r2;
+        ci2[e + 3 * nthreads] = r3;
+    }
+    for (; e < arcs; e += nthreads) ci2[e] = rl_rank2(bw, ld_stream(ci + e, cold));
 }
 
 __global__ void rl_back_kernel(const unsigned *bits, const unsigned *wpre, const int *core2, long long n,
@@ -94,6 +114,7 @@ size_t relabel_workspace_bytes(long long n, long long arcs) {
     long long nw = (n + 31) / 32;
     size_t b = 0;
     b += a256(sizeof(unsigned) * (size_t)nw) * 3;       // bits, wcnt, wpre
+    b += a256(sizeof(uint2) * (size_t)nw);              // (bits, wpre) packed
     b += a256(sizeof(long long) * (size_t)(n + 1));     // rp2
     b += a256(sizeof(int) * (size_t)n);                 // inv
     b += a256(sizeof(int) * (size_t)arcs);              // ci2
@@ -109,6 +130,7 @@ cudaError_t relabel_build(const long long *rp, const int *ci, long long n, long 
     unsigned *bits = (unsigned *)p; p += a256(sizeof(unsigned) * (size_t)nw);
     unsigned *wcnt = (unsigned *)p; p += a256(sizeof(unsigned) * (size_t)nw);
     unsigned *wpre = (unsigned *)p; p += a256(sizeof(unsigned) * (size_t)nw);
+    uint2 *bw = (uint2 *)p; p += a256(sizeof(uint2) * (size_t)nw);
     long long *rp2 = (long long *)p; p += a256(sizeof(long long) * (size_t)(n + 1));
     int *inv = (int *)p; p += a256(sizeof(int) * (size_t)n);
     int *ci2 = (int *)p; p += a256(sizeof(int) * (size_t)arcs);
@@ -131,7 +153,8 @@ cudaError_t relabel_build(const long long *rp, const int *ci, long long n, long 
     out->active = force || out->n2 * 10 < n * 9;
     if (!out->active) return cudaGetLastError();
     rl_rows_kernel<<<grid(n), 256, 0, s>>>(rp, n, bits, wpre, rp2, inv, arcs);
-    rl_arcs_kernel<<<grid(arcs), 256, 0, s>>>(ci, arcs, bits, wpre, ci2);
+    rl_pack_kernel<<<grid(nw), 256, 0, s>>>(bits, wpre, nw, bw);
+    rl_arcs_kernel<<<dev.sms * 16, 256, 0, s>>>(ci, arcs, bw, ci2);
     if ((e = cudaGetLastError())) return e;
     out->rp2 = rp2;
     out->ci2 = ci2;
@@ -139,7 +162,7 @@ cudaError_t relabel_build(const long long *rp, const int *ci, long long n, long 
     out->wpre = wpre;
     out->inv = inv;
     out->core2 = core2;
-    out->launches = 4;
+    out->launches = 5;
     return cudaSuccess;
 }
 

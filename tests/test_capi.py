@@ -163,3 +163,36 @@ def test_host_entry_point_matches_device():
         st = pico.Stats()
         core = pico.coreness_host(rp, ci, algo=algo, stats=st)
         assert np.array_equal(core, ref)
+
+
+@pytest.mark.gpu
+def test_invalid_graph_terminates():
+    """An input that breaks the CSR contract (asymmetric, duplicate arcs) is
+    not validated by default, but the call must still return -- a status or
+    some coreness -- instead of hanging the device."""
+    import torch
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(3)
+    n = 2000
+    deg = rng.integers(0, 40, n)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(deg)
+    ci = rng.integers(0, n, rp[-1]).astype(np.int32)  # random one-way arcs with repeats
+    if ci.size % 2:
+        ci = ci[:-1]
+        rp[-1] -= 1
+        rp = np.minimum(rp, ci.size)
+    r = torch.from_numpy(rp).to(dev)
+    c = torch.from_numpy(ci).to(dev)
+    for algo in ("histocore", "peelone"):
+        for fl in (0, pico.F_PULL_ALWAYS, pico.F_PUSH_ONLY):
+            if algo == "peelone" and fl:
+                continue
+            try:
+                pico.coreness(r, c, algo=algo, flags=fl)
+                torch.cuda.synchronize()
+            except pico.PicoError as e:
+                assert e.status in (4, 6)
+    with pytest.raises(pico.PicoError) as ei:
+        pico.coreness(r, c, flags=pico.F_VALIDATE)
+    assert ei.value.status == 6
