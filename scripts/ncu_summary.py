@@ -1,11 +1,11 @@
 #!/usr/bin/env python
 """Summarise ncu captures of one bench step into profiles/.
 
-    python scripts/ncu_summary.py CONFIG ALGO REPORT.ncu-rep [--out profiles/ncu_traffic.json]
+    python scripts/ncu_summary.py CONFIG ALGO REPORT.ncu-rep|RAW.csv [--out profiles/ncu_traffic.json]
                                   [--md profiles/r01/ncu_CONFIG_ALGO.md]
 
 Maps kernels to bench.py's kernel slots (degree / init / rounds / peel /
-relabel), sums dram__bytes_read.sum + dram__bytes_write.sum and
+edgelist / relabel), sums dram__bytes_read.sum + dram__bytes_write.sum and
 gpu__time_duration.sum per slot (one step = one launch of every slot kernel),
 merges the per-slot DRAM bytes into the JSON that bench.py reports as
 roofline.traffic, and writes a human-readable table of the key metrics.
@@ -21,7 +21,8 @@ SLOTS = [
     ("init", ("hc_init_small", "hc_init_warp", "hc_init_cta", "hc_init_fallback", "hc_shadow")),
     ("degree", ("hc_degree_kernel", "po_init_kernel")),
     ("peel", ("po_levels_kernel",)),
-    ("relabel", ("rl_bits", "rl_rows", "rl_arcs", "rl_back", "DeviceScan")),
+    ("edgelist", ("hc_el_",)),
+    ("relabel", ("rl_bits", "rl_rows", "rl_pack", "rl_arcs", "rl_back", "DeviceScan")),
 ]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -47,7 +48,10 @@ def main():
         out = sys.argv[sys.argv.index("--out") + 1]
     if "--md" in sys.argv:
         md = sys.argv[sys.argv.index("--md") + 1]
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a raw page exported on the GPU box (ncu -i REP --page raw --csv)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     agg, lines, seen = {}, [], set()
@@ -90,7 +94,7 @@ def main():
         json.dump(allj, f, indent=1, sort_keys=True)
     if md:
         with open(md, "w") as f:
-            f.write(f"# ncu --set full summary: {cfg} {algo} ({rep})\n\n")
+            f.write(f"# ncu --set full summary: {cfg}, one HistoCore and one PeelOne call ({rep})\n\n")
             f.write("ncu replays each kernel with cold caches and serialised launches: times are for shares, "
                     "not absolutes.\n\n")
             f.write("| kernel | slot | time ms | DRAM read GB | DRAM write GB | L2 hit % | warps active % | L2 thru % | regs |\n")

@@ -72,9 +72,14 @@ def hash_u32(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
 # ----------------------------------------------------------------------------
 # CSR construction
 # ----------------------------------------------------------------------------
+_SORT_LIM = 1 << 30  # torch.sort handles at most INT_MAX elements per call
+
+
 def csr_from_edges(n: int, src: torch.Tensor, dst: torch.Tensor):
     """Symmetrize, drop self loops, dedup, sort rows ascending -> CSR.
-    Returns (rowptr int64[n+1], colidx int32[2m]) on src's device."""
+    Returns (rowptr int64[n+1], colidx int32[2m]) on src's device.  Graphs
+    with more than 2^30 arcs are sorted in row ranges (same result: the
+    global order of the (row, col) keys is the concatenation of the ranges')."""
     dev = src.device
     src = src.to(torch.int64)
     dst = dst.to(torch.int64)
@@ -82,13 +87,20 @@ def csr_from_edges(n: int, src: torch.Tensor, dst: torch.Tensor):
     src, dst = src[keep], dst[keep]
     keys = torch.cat([src * n + dst, dst * n + src])
     del src, dst, keep
-    keys = torch.sort(keys).values
-    keys = torch.unique_consecutive(keys)
-    rows = keys // n
-    colidx = (keys - rows * n).to(torch.int32)
+    nparts = max(1, -(-keys.numel() // (_SORT_LIM // 2)))
+    counts = torch.zeros(n, dtype=torch.int64, device=dev)
+    cols = []
+    for q in range(nparts):
+        lo, hi = n * q // nparts, n * (q + 1) // nparts
+        part = keys if nparts == 1 else keys[(keys >= lo * n) & (keys < hi * n)]
+        part = torch.unique_consecutive(torch.sort(part).values)
+        rows = part // n
+        cols.append((part - rows * n).to(torch.int32))
+        counts += torch.bincount(rows, minlength=n)
+        del part, rows
     del keys
-    counts = torch.bincount(rows, minlength=n)
-    del rows
+    colidx = cols[0] if len(cols) == 1 else torch.cat(cols)
+    del cols
     rowptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     rowptr[1:] = torch.cumsum(counts, 0)
     return rowptr, colidx
@@ -98,11 +110,13 @@ def compact_isolated(rowptr: torch.Tensor, colidx: torch.Tensor):
     """Drop degree-0 vertices and renumber the rest in order."""
     deg = rowptr[1:] - rowptr[:-1]
     keep = deg > 0
-    newid = torch.cumsum(keep.to(torch.int64), 0) - 1
+    newid = (torch.cumsum(keep.to(torch.int64), 0) - 1).to(torch.int32)
     n2 = int(keep.sum().item())
     rp = torch.zeros(n2 + 1, dtype=torch.int64, device=rowptr.device)
     rp[1:] = torch.cumsum(deg[keep], 0)
-    ci = newid[colidx.to(torch.int64)].to(torch.int32)
+    ci = torch.empty_like(colidx)
+    for s0 in range(0, colidx.numel(), _SORT_LIM):  # gathers in < INT_MAX chunks
+        ci[s0:s0 + _SORT_LIM] = newid[colidx[s0:s0 + _SORT_LIM].to(torch.int64)]
     return rp, ci
 
 
