@@ -8,8 +8,9 @@
  *
  *     pico_shard_pack   -> this rank's changed (v, oldcore, core) triples
  *     allgatherv        -> every rank receives every rank's triples
- *                          (done by the caller, e.g. torch.distributed /
- *                          NCCL: paper_2402_15253_b200/sharded.py)
+ *                          (done by the caller, e.g. torch.distributed:
+ *                          paper_2402_15253_b200/sharded.py, or inside the
+ *                          library over NCCL: pico_coreness_sharded below)
  *     pico_shard_apply  -> UpdateHisto of all received triples over the
  *                          local CSC (owned neighbours of each v), then
  *                          SumHisto of the local frontier
@@ -70,6 +71,51 @@ int pico_shard_apply(pico_shard_t h, const int32_t *triples, int64_t total, int6
 int pico_shard_result(pico_shard_t h, int32_t *core_local);
 
 int pico_shard_destroy(pico_shard_t h);
+
+/* ------------------------------------------------------------------------
+ * One-call sharded coreness with the exchange inside the library (NCCL over
+ * NVLink/NVSwitch).  One process (or thread) per GPU.
+ * libnccl.so.2 is loaded on first use (dlopen); if it cannot be loaded the
+ * comm calls return PICO_ENCCL.  NCCL errors -> PICO_ENCCL.
+ * ---------------------------------------------------------------------- */
+typedef struct pico_comm_s *pico_comm_t;
+
+/* id (host, 128 bytes) <- a fresh NCCL unique id; call on one rank and
+ * broadcast it to the others (e.g. through torch.distributed). */
+int pico_comm_unique_id(uint8_t id[128]);
+
+/* *comm <- communicator of rank `rank` of `nranks` on the CURRENT CUDA device
+ * (ncclCommInitRank; collective over all ranks). */
+int pico_comm_init(int nranks, int rank, const uint8_t id[128], pico_comm_t *comm);
+
+/* Rank count / rank of a communicator (NULL comm -> PICO_EINVAL). */
+int pico_comm_size(pico_comm_t comm, int *nranks, int *rank);
+
+/* Coreness of the owned vertices [v_begin, v_end) of a graph whose rows are
+ * split over the communicator's ranks in rank order (rank r's range starts
+ * where rank r-1's ends; they tile [0, n_global)).  rowptr_local [nloc+1]
+ * (int64, rowptr_local[0] = 0, nloc = v_end - v_begin) and colidx_local
+ * (int32 GLOBAL ids) are DEVICE arrays of the owned rows; core_out_local
+ * (device int32 [nloc]) receives their coreness.  m_global = undirected edges
+ * of the whole graph (the local arc counts must sum to 2 m_global, else
+ * PICO_EINVAL on every rank).  algo: PICO_ALGO_HISTOCORE (PeelOne is not
+ * sharded: PICO_ENOTSUP).  Collective and blocking: every rank calls it with
+ * its own range; the per-round exchange is an all-gather of the changed-triple
+ * counts (the global convergence test) and a grouped-broadcast all-gatherv of
+ * the (v, oldcore, core) triples, both on `stream`. */
+int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
+                          int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
+                          int32_t *core_out_local, pico_stream_t stream);
+
+/* Same with PICO_F_* schedule flags and optional stats (rounds = l2 and,
+ * when stats->frontier_sizes is set, the GLOBAL |C_t| per round, identical
+ * on every rank). */
+int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
+                             int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
+                             int32_t *core_out_local, pico_stream_t stream, uint32_t flags,
+                             pico_stats_t *stats);
+
+int pico_comm_destroy(pico_comm_t comm);
 
 #ifdef __cplusplus
 }

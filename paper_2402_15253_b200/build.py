@@ -19,6 +19,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC", "-shared",
     "-Xcompiler", "-fvisibility=default",
+    "-ldl",  # NCCL is loaded with dlopen by the sharded entry points
 ]
 
 

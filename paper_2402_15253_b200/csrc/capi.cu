@@ -439,3 +439,240 @@ int pico_shard_destroy(pico_shard_t h) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// One-call sharded HistoCore with the exchange inside the library (NCCL,
+// loaded with dlopen on first use; include/pico_shard.h).  The round loop is
+// that of paper_2402_15253_b200/sharded.py: pack -> all-gather of the counts
+// (global convergence test) -> all-gatherv of the triples (grouped
+// broadcasts) -> apply.
+// ===========================================================================
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only: the symbols come from dlopen
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi load_nccl() {
+    NcclApi a;
+    const char *env = getenv("PICO_NCCL_LIB");
+    void *h = nullptr;
+    for (const char *name : {env, "libnccl.so.2", "libnccl.so"}) {
+        if (!name) continue;
+        h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) {
+        a.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+        return a;
+    }
+#define PICO_SYM(f)                                                     \
+    *(void **)(&a.f) = dlsym(h, "nccl" #f);                             \
+    if (!a.f) {                                                         \
+        a.err = "libnccl lacks nccl" #f;                                \
+        return a;                                                       \
+    }
+    PICO_SYM(GetUniqueId)
+    PICO_SYM(CommInitRank)
+    PICO_SYM(CommDestroy)
+    PICO_SYM(AllGather)
+    PICO_SYM(Broadcast)
+    PICO_SYM(GroupStart)
+    PICO_SYM(GroupEnd)
+    PICO_SYM(GetErrorString)
+#undef PICO_SYM
+    a.ok = true;
+    return a;
+}
+
+NcclApi &nccl() {
+    static NcclApi api = load_nccl();  // thread-safe initialisation
+    return api;
+}
+
+}  // namespace
+
+struct pico_comm_s {
+    ncclComm_t c;
+    int nranks, rank;
+};
+
+static int nccl_fail(ncclResult_t r, const char *where) {
+    return fail(PICO_ENCCL, "%s: %s", where, nccl().GetErrorString ? nccl().GetErrorString(r) : "NCCL error");
+}
+
+extern "C" {
+
+int pico_comm_unique_id(uint8_t id[128]) {
+    g_last_error.clear();
+    if (!id) return fail(PICO_EINVAL, "NULL id");
+    if (!nccl().ok) return fail(PICO_ENCCL, "%s", nccl().err.c_str());
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId u;
+    ncclResult_t r = nccl().GetUniqueId(&u);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(id, &u, 128);
+    return PICO_OK;
+}
+
+int pico_comm_init(int nranks, int rank, const uint8_t id[128], pico_comm_t *comm) {
+    g_last_error.clear();
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(PICO_EINVAL, "bad argument");
+    *comm = nullptr;
+    if (!nccl().ok) return fail(PICO_ENCCL, "%s", nccl().err.c_str());
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclComm_t c;
+    ncclResult_t r = nccl().CommInitRank(&c, nranks, u, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+    *comm = new pico_comm_s{c, nranks, rank};
+    return PICO_OK;
+}
+
+int pico_comm_size(pico_comm_t comm, int *nranks, int *rank) {
+    g_last_error.clear();
+    if (!comm) return fail(PICO_EINVAL, "NULL comm");
+    if (nranks) *nranks = comm->nranks;
+    if (rank) *rank = comm->rank;
+    return PICO_OK;
+}
+
+int pico_comm_destroy(pico_comm_t comm) {
+    g_last_error.clear();
+    if (!comm) return PICO_OK;
+    ncclResult_t r = nccl().CommDestroy(comm->c);
+    delete comm;
+    return r == ncclSuccess ? PICO_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
+                             int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
+                             int32_t *core_out_local, pico_stream_t stream, uint32_t flags,
+                             pico_stats_t *stats) {
+    g_last_error.clear();
+    reset_stats(stats);
+    if (!comm) return fail(PICO_EINVAL, "NULL comm");
+    if (algo == PICO_ALGO_PEELONE) return fail(PICO_ENOTSUP, "PeelOne is not sharded (replicas only)");
+    if (algo != PICO_ALGO_HISTOCORE) return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (v_begin < 0 || v_end < v_begin || v_end > n_global || n_global <= 0 || m_global < 0)
+        return fail(PICO_EINVAL, "bad range [%lld, %lld) of %lld", (long long)v_begin, (long long)v_end,
+                    (long long)n_global);
+    if (n_global >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n_global needs 64-bit vertex ids");
+    if (!rowptr_local || (v_end > v_begin && !core_out_local)) return fail(PICO_EINVAL, "NULL pointer");
+    const long long nloc = v_end - v_begin;
+    const int P = comm->nranks, me = comm->rank;
+    cudaStream_t s = (cudaStream_t)stream;
+    NcclApi &N = nccl();
+    DevInfo dev;
+    cudaError_t e = dev_info(&dev);
+    if (e) return cuda_fail(e, "device query");
+
+    Shard *sh = nullptr;
+    e = shard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags, s, dev, &sh);
+    if (e) return cuda_fail(e, "shard create");
+    // device scratch: meta [3 + 3P] int64, counts [1 + P] int64, degrees, triples
+    long long *meta = nullptr, *cnt = nullptr;
+    int *deg_g = nullptr, *trip = nullptr, *all = nullptr;
+    size_t all_cap = 0;
+    int rc = PICO_OK;
+    ncclResult_t nr;
+    std::vector<long long> hm(3 * P), hc(P);
+    std::vector<long long> off(P + 1, 0);
+    auto bail_cuda = [&](cudaError_t err, const char *w) { rc = cuda_fail(err, w); };
+    auto bail_nccl = [&](ncclResult_t r, const char *w) { rc = nccl_fail(r, w); };
+    do {
+        if ((e = cudaMallocAsync((void **)&meta, sizeof(long long) * (3 + 3 * P), s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = cudaMallocAsync((void **)&cnt, sizeof(long long) * (1 + P), s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = cudaMallocAsync((void **)&deg_g, sizeof(int) * (size_t)n_global, s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = cudaMallocAsync((void **)&trip, sizeof(int) * 3 * (size_t)std::max(nloc, 1ll), s))) {
+            bail_cuda(e, "alloc");
+            break;
+        }
+        // every rank's (v_begin, v_end, local arcs): the ranges must tile [0, n_global) in rank order
+        long long mine[3] = {v_begin, v_end, 0};
+        if ((e = cudaMemcpyAsync(&mine[2], rowptr_local + nloc, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
+            (e = cudaStreamSynchronize(s))) { bail_cuda(e, "local arcs"); break; }
+        if ((e = cudaMemcpyAsync(meta, mine, sizeof(mine), cudaMemcpyHostToDevice, s))) { bail_cuda(e, "meta"); break; }
+        if ((nr = N.AllGather(meta, meta + 3, 3, ncclInt64, comm->c, s)) != ncclSuccess) { bail_nccl(nr, "allgather ranges"); break; }
+        if ((e = cudaMemcpyAsync(hm.data(), meta + 3, sizeof(long long) * 3 * P, cudaMemcpyDeviceToHost, s)) ||
+            (e = cudaStreamSynchronize(s))) { bail_cuda(e, "ranges"); break; }
+        long long arcs = 0;
+        bool tiled = hm[0] == 0 && hm[3 * (P - 1) + 1] == n_global;
+        for (int r = 0; r < P; r++) {
+            arcs += hm[3 * r + 2];
+            if (r > 0 && hm[3 * r] != hm[3 * (r - 1) + 1]) tiled = false;
+        }
+        if (!tiled) { rc = fail(PICO_EINVAL, "rank ranges do not tile [0, n_global) in rank order"); break; }
+        if (arcs != 2 * m_global) { rc = fail(PICO_EINVAL, "local arcs sum to %lld, not 2m = %lld", arcs, 2 * (long long)m_global); break; }
+        // degrees: all-gatherv into deg_global
+        if ((e = shard_degrees(sh, deg_g + v_begin))) { bail_cuda(e, "shard degrees"); break; }
+        if ((nr = N.GroupStart()) != ncclSuccess) { bail_nccl(nr, "group"); break; }
+        for (int r = 0; r < P && nr == ncclSuccess; r++) {
+            long long c = hm[3 * r + 1] - hm[3 * r];
+            if (c > 0) nr = N.Broadcast(deg_g + hm[3 * r], deg_g + hm[3 * r], (size_t)c, ncclInt32, r, comm->c, s);
+        }
+        ncclResult_t ne = N.GroupEnd();
+        if (nr != ncclSuccess || ne != ncclSuccess) { bail_nccl(nr != ncclSuccess ? nr : ne, "allgatherv degrees"); break; }
+        long long changed = 0;
+        if ((e = shard_init(sh, deg_g, &changed))) { bail_cuda(e, "shard init"); break; }
+        // rounds
+        long long rounds = 0;
+        for (;;) {
+            long long c = 0;
+            if ((e = shard_pack(sh, trip, std::max(nloc, 1ll), &c))) { bail_cuda(e, "shard pack"); break; }
+            if ((e = cudaMemcpyAsync(cnt, &c, sizeof(long long), cudaMemcpyHostToDevice, s))) { bail_cuda(e, "count"); break; }
+            if ((nr = N.AllGather(cnt, cnt + 1, 1, ncclInt64, comm->c, s)) != ncclSuccess) { bail_nccl(nr, "allgather counts"); break; }
+            if ((e = cudaMemcpyAsync(hc.data(), cnt + 1, sizeof(long long) * P, cudaMemcpyDeviceToHost, s)) ||
+                (e = cudaStreamSynchronize(s))) { bail_cuda(e, "counts"); break; }
+            for (int r = 0; r < P; r++) off[r + 1] = off[r] + hc[r];
+            const long long total = off[P];
+            if (total == 0) break;  // global convergence
+            if (stats && stats->frontier_sizes && rounds < stats->frontier_sizes_cap)
+                stats->frontier_sizes[rounds] = total;
+            rounds++;
+            if ((size_t)(3 * total) > all_cap) {
+                if (all) cudaFreeAsync(all, s);
+                all_cap = (size_t)(3 * total) + (size_t)(3 * total) / 4;
+                if ((e = cudaMallocAsync((void **)&all, sizeof(int) * all_cap, s))) { all = nullptr; bail_cuda(e, "alloc"); break; }
+            }
+            if ((nr = N.GroupStart()) != ncclSuccess) { bail_nccl(nr, "group"); break; }
+            for (int r = 0; r < P && nr == ncclSuccess; r++)
+                if (hc[r] > 0)
+                    nr = N.Broadcast(r == me ? (const void *)trip : (const void *)(all + 3 * off[r]), all + 3 * off[r],
+                                     (size_t)(3 * hc[r]), ncclInt32, r, comm->c, s);
+            ne = N.GroupEnd();
+            if (nr != ncclSuccess || ne != ncclSuccess) { bail_nccl(nr != ncclSuccess ? nr : ne, "allgatherv triples"); break; }
+            if ((e = shard_apply(sh, all, total, nullptr))) { bail_cuda(e, "shard apply"); break; }
+        }
+        if (rc != PICO_OK) break;
+        if (stats) stats->rounds = rounds;
+        if (nloc > 0 && (e = shard_result(sh, core_out_local))) { bail_cuda(e, "shard result"); break; }
+    } while (false);
+    cudaError_t ed = shard_destroy(sh);
+    for (void *ptr : {(void *)meta, (void *)cnt, (void *)deg_g, (void *)trip, (void *)all})
+        if (ptr) cudaFreeAsync(ptr, s);
+    cudaError_t es = cudaStreamSynchronize(s);
+    if (rc == PICO_OK && (ed || es)) rc = cuda_fail(ed ? ed : es, "sharded cleanup");
+    return rc;
+}
+
+int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
+                          int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
+                          int32_t *core_out_local, pico_stream_t stream) {
+    return pico_coreness_sharded_ex(comm, rowptr_local, colidx_local, n_global, m_global, v_begin, v_end, algo,
+                                    core_out_local, stream, 0, nullptr);
+}
+
+}  // extern "C"
