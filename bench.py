@@ -387,6 +387,8 @@ def main():
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-both", dest="both", action="store_false")
     ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
+                    help="sharded path: NCCL inside libpico (pico_coreness_sharded) or torch.distributed")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded path even at one rank (torchrun --nproc-per-node 1)")
     args = ap.parse_args()

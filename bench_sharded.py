@@ -30,6 +30,7 @@ def bench_sharded(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
@@ -42,12 +43,21 @@ def bench_sharded(args):
     vb, ve = bounds[rank], bounds[rank + 1]
     rp_l, ci_l = sharded.local_rows(rp, ci, vb, ve)
 
-    def step():
-        shard = sharded.DeviceShard(rp_l, ci_l, vb, n, args.flags)
+    comm = sharded.NcclComm() if args.exchange == "nccl" else None
+
+    def run_once(rp_d, ci_d):
+        if comm is not None:  # one library call; the exchange runs over NCCL inside libpico
+            r = sharded.coreness_sharded_nccl(rp_d, ci_d, n, m, vb, comm, flags=args.flags)
+            r.triples_exchanged = sum(r.frontier_sizes)
+            return r
+        shard = sharded.DeviceShard(rp_d, ci_d, vb, n, args.flags)
         try:
             return sharded.run_shard(shard, ex, dev)
         finally:
             shard.close()
+
+    def step():
+        return run_once(rp_l, ci_l)
 
     for _ in range(args.warmup):
         run = step()
@@ -97,11 +107,7 @@ def bench_sharded(args):
     for _ in range(e2e_steps):
         rp_d = rp_h.to(dev, non_blocking=True)
         ci_d = ci_h.to(dev, non_blocking=True)
-        shard = sharded.DeviceShard(rp_d, ci_d, vb, n, args.flags)
-        try:
-            r2 = sharded.run_shard(shard, ex, dev)
-        finally:
-            shard.close()
+        r2 = run_once(rp_d, ci_d)
         out_h[:r2.core_local.numel()].copy_(r2.core_local, non_blocking=True)
         torch.cuda.synchronize()
     dist.barrier()
@@ -115,7 +121,9 @@ def bench_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": cfg.note, "config": args.config, "algo": "histocore-sharded", "n": n, "m": m,
-                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL)",
+                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL, "
+                                      + ("inside libpico: pico_coreness_sharded)" if comm is not None
+                                         else "torch.distributed)"),
                        "l2_flush": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
                          "traffic": None, "peak_source": src + f" x {world} GPUs",
@@ -132,5 +140,7 @@ def bench_sharded(args):
         }
         print(json.dumps(out), flush=True)
     dist.barrier()
+    if comm is not None:
+        comm.close()
     dist.destroy_process_group()
     return 0

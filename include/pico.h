@@ -59,7 +59,11 @@ typedef struct CUstream_st *pico_stream_t;
 
 typedef enum {
     PICO_ALGO_HISTOCORE = 0, /* Alg 6, P:489-539 (primary kernel)           */
-    PICO_ALGO_PEELONE = 1    /* Alg 4 + dynamic frontier       */
+    PICO_ALGO_PEELONE = 1,   /* Alg 4 + dynamic frontier       */
+    PICO_ALGO_AUTO = 2       /* pick one of the two from the degree skew  */
+                             /* d_max * n / 2m and the size 2m (SURVEY    */
+                             /* 8(f) NEXT-2; rule and data: DESIGN.md);   */
+                             /* stats->algo reports the choice            */
 } pico_algo_t;
 
 typedef enum {
@@ -158,6 +162,8 @@ typedef struct {
      * of the SumHisto that builds F_{t+1} at [2(t-1)+1]; may be NULL.  Filled
      * by the persistent round kernel only (not PICO_F_HOST_LOOP). */
     int64_t *round_ns;
+    /* the algorithm that ran (PICO_ALGO_AUTO resolved) */
+    int64_t algo;
 } pico_stats_t;
 
 /* The north-star entry point: coreness of every vertex, device buffers. */

@@ -10,7 +10,7 @@ import re
 
 from .build import INCLUDE, LIB
 
-ALGOS = {"histocore": 0, "peelone": 1}
+ALGOS = {"histocore": 0, "peelone": 1, "auto": 2}
 
 F_VALIDATE = 1
 F_STATS = 2
@@ -63,10 +63,12 @@ class Stats(ctypes.Structure):
         ("frontier_sizes_cap", ctypes.c_int64),
         ("round_arcs", ctypes.POINTER(ctypes.c_int64)),
         ("round_ns", ctypes.POINTER(ctypes.c_int64)),
+        ("algo", ctypes.c_int64),
     ]
 
     def to_dict(self) -> dict:
         d = {k: int(getattr(self, k)) for k, _ in self._fields_[:16]}
+        d["algo"] = int(self.algo)
         d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(9) if self.kernel_launches[i]}
         d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(9) if self.kernel_launches[i]}
         return d
@@ -141,6 +143,21 @@ def _setup_shard(lib):
     lib.pico_shard_result.restype = i32
     lib.pico_shard_destroy.argtypes = [vp]
     lib.pico_shard_destroy.restype = i32
+    if hasattr(lib, "pico_coreness_sharded"):
+        u8p = ctypes.POINTER(ctypes.c_uint8)
+        lib.pico_comm_unique_id.argtypes = [u8p]
+        lib.pico_comm_unique_id.restype = i32
+        lib.pico_comm_init.argtypes = [i32, i32, u8p, ctypes.POINTER(vp)]
+        lib.pico_comm_init.restype = i32
+        lib.pico_comm_size.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        lib.pico_comm_size.restype = i32
+        lib.pico_comm_destroy.argtypes = [vp]
+        lib.pico_comm_destroy.restype = i32
+        lib.pico_coreness_sharded.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, vp]
+        lib.pico_coreness_sharded.restype = i32
+        lib.pico_coreness_sharded_ex.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, vp, u32,
+                                                 ctypes.POINTER(Stats)]
+        lib.pico_coreness_sharded_ex.restype = i32
 
 
 def check(rc: int):

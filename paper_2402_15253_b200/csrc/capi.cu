@@ -170,7 +170,40 @@ static bool use_relabel(long long n, long long m, uint32_t flags) {
 static size_t algo_bytes(long long n, long long arcs, int algo, uint32_t flags) {
     if (algo == PICO_ALGO_HISTOCORE) return hc_workspace_bytes(n, arcs, flags);
     if (algo == PICO_ALGO_PEELONE) return po_workspace_bytes(n, arcs, flags);
+    if (algo == PICO_ALGO_AUTO)
+        return std::max(hc_workspace_bytes(n, arcs, flags), po_workspace_bytes(n, arcs, flags));
     return 0;
+}
+
+// PICO_ALGO_AUTO: HistoCore on skewed graphs of moderate
+// size, PeelOne otherwise.  Measured on B200 over RMAT / flat-Kronecker
+// graphs of 2^12..2^22 vertices (scripts/algo_sweep.py):
+// HistoCore wins where the degree skew d_max * n / 2m is high and the graph
+// small enough that its dense rounds are cheap; PeelOne wins on flat graphs
+// (few levels) and on large ones (its one pass over the arcs).
+constexpr double kAutoSkew = 60.0;
+constexpr long long kAutoMaxArcs = 64ll << 20;
+
+__global__ void deg_max_kernel(const long long *rp, long long n, int *out) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    int m = 0;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nthreads)
+        m = max(m, (int)(rp[v + 1] - rp[v]));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+static cudaError_t auto_select(const long long *rp, long long n, long long arcs, cudaStream_t s, void *scratch,
+                               const DevInfo &dev, int *algo) {
+    int *d = (int *)scratch, dmax = 0;
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(int), s);
+    if (e) return e;
+    deg_max_kernel<<<dev.sms * 4, 256, 0, s>>>(rp, n, d);
+    if ((e = cudaMemcpyAsync(&dmax, d, sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    double skew = arcs > 0 ? (double)dmax * (double)n / (double)arcs : 0.0;
+    *algo = (skew >= kAutoSkew && arcs <= kAutoMaxArcs) ? PICO_ALGO_HISTOCORE : PICO_ALGO_PEELONE;
+    return cudaGetLastError();
 }
 
 size_t pico_workspace_bytes(int64_t n, int64_t m, int algo, uint32_t flags) {
@@ -188,8 +221,9 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
     g_last_error.clear();
     reset_stats(stats);
     if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n (%lld) or m (%lld)", (long long)n, (long long)m);
-    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE)
+    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE && algo != PICO_ALGO_AUTO)
         return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (stats) stats->algo = algo == PICO_ALGO_AUTO ? PICO_ALGO_HISTOCORE : algo;
     if (n == 0) return PICO_OK;
     if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n = %lld needs 64-bit vertex ids", (long long)n);
     if (!rowptr || !core_out || (m > 0 && !colidx)) return fail(PICO_EINVAL, "NULL pointer argument");
@@ -220,6 +254,14 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
             rc = fail(PICO_EGRAPH, "graph violates the CSR contract (flags 0x%x: %s%s%s%s%s)", bad,
                       (bad & 1) ? "rowptr " : "", (bad & 2) ? "range " : "", (bad & 4) ? "self-loop " : "",
                       (bad & 8) ? "unsorted/duplicate " : "", (bad & 16) ? "asymmetric" : "");
+    }
+    if (rc == PICO_OK && algo == PICO_ALGO_AUTO && m > 0) {
+        e = auto_select(rp, n, arcs, s, ws, dev, &algo);
+        if (e) rc = cuda_fail(e, "auto select");
+        if (stats) {
+            stats->algo = algo;
+            stats->kernel_count += 1;
+        }
     }
     if (rc == PICO_OK) {
         if (m == 0) {
@@ -320,7 +362,7 @@ int pico_coreness_host(const int64_t *rowptr_h, const int32_t *colidx_h, int64_t
     g_last_error.clear();
     reset_stats(stats);
     if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n or m");
-    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE)
+    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE && algo != PICO_ALGO_AUTO)
         return fail(PICO_EINVAL, "unknown algo %d", algo);
     if (n == 0) return PICO_OK;
     if (!rowptr_h || !core_out_h || (m > 0 && !colidx_h)) return fail(PICO_EINVAL, "NULL pointer argument");

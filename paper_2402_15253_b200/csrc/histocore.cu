@@ -1557,7 +1557,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     if ((err = cudaGetLastError())) return err;
     if (st) {
         st->rounds = (int64_t)rounds;
-        st->kernel_count = launches;
+        st->kernel_count += launches;
         st->segments_init = (int64_t)s1;
         if (st->frontier_sizes)
             for (size_t i = 0; i < hsz.size() && (int64_t)i < st->frontier_sizes_cap; i++)

@@ -411,7 +411,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         st->subrounds = (flags & PICO_F_HOST_LOOP) ? host_subrounds : (int64_t)hc.rounds;
         st->kmax = hc.kmax;
         st->segments = (int64_t)hc.q_tail;
-        st->kernel_count = launches;
+        st->kernel_count += launches;
         if (st->frontier_sizes)
             for (unsigned long long i = 0; i < hc.levels && (int64_t)i < st->frontier_sizes_cap && i < kFszCap; i++)
                 st->frontier_sizes[i] = (int64_t)lv[i];

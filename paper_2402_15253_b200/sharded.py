@@ -210,6 +210,71 @@ def coreness_sharded(rowptr, colidx, group=None, flags: int = 0) -> ShardRun:
 
 
 # ---------------------------------------------------------------------------
+# one-call path: the exchange inside libpico over NCCL (pico_coreness_sharded)
+# ---------------------------------------------------------------------------
+class NcclComm:
+    """libpico's NCCL communicator (pico_comm_t) on the current CUDA device.
+    The unique id is made on rank 0 and broadcast through the given
+    torch.distributed group (or pass nranks=1 for a single rank)."""
+
+    def __init__(self, group=None, nranks: int | None = None, rank: int = 0):
+        import torch
+        self.lib = load()
+        if nranks is None:
+            import torch.distributed as dist
+            nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            check(self.lib.pico_comm_unique_id(uid))
+        if nranks > 1:
+            import torch.distributed as dist
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        h = ctypes.c_void_p()
+        check(self.lib.pico_comm_init(nranks, rank, uid, ctypes.byref(h)))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if self.h:
+            check(self.lib.pico_comm_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coreness_sharded_nccl(rowptr_local, colidx_local, n_global: int, m_global: int, v_begin: int,
+                          comm: NcclComm, flags: int = 0, algo: int = 0, stream=None, frontier_cap: int = 1 << 16):
+    """Sharded HistoCore of this rank's rows [v_begin, v_begin + nloc) in ONE
+    library call (pico_coreness_sharded_ex): the per-round exchange runs over
+    NCCL inside libpico.  Returns a ShardRun (core_local, rounds, global |C_t|)."""
+    import torch
+    from ._lib import Stats
+    lib = load()
+    dev = rowptr_local.device
+    nloc = rowptr_local.numel() - 1
+    stream = stream or torch.cuda.current_stream(dev)
+    out = torch.empty(max(nloc, 1), dtype=torch.int32, device=dev)
+    st = Stats()
+    fs = np.zeros(frontier_cap, dtype=np.int64)
+    st.frontier_sizes = fs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    st.frontier_sizes_cap = frontier_cap
+    check(lib.pico_coreness_sharded_ex(comm.h, rowptr_local.data_ptr(),
+                                       colidx_local.data_ptr() if colidx_local.numel() else None, n_global, m_global,
+                                       v_begin, v_begin + nloc, algo, out.data_ptr() if nloc else None,
+                                       ctypes.c_void_p(stream.cuda_stream), flags, ctypes.byref(st)))
+    run = ShardRun(core_local=out[:nloc], rounds=int(st.rounds))
+    run.frontier_sizes = [int(x) for x in fs[:run.rounds]]
+    return run
+
+
+# ---------------------------------------------------------------------------
 # loopback: P logical shards on one GPU (parity of the sharded kernels)
 # ---------------------------------------------------------------------------
 def coreness_loopback(rowptr, colidx, nparts: int, flags: int = 0):

@@ -196,3 +196,16 @@ def test_invalid_graph_terminates():
     with pytest.raises(pico.PicoError) as ei:
         pico.coreness(r, c, flags=pico.F_VALIDATE)
     assert ei.value.status == 6
+
+
+def test_sharded_abi_argument_checks():
+    """The NCCL sharded entry points reject bad arguments without a GPU."""
+    lib = pico.load()
+    uid = (ctypes.c_uint8 * 128)()
+    h = ctypes.c_void_p()
+    assert lib.pico_comm_init(0, 0, uid, ctypes.byref(h)) == 1       # nranks < 1
+    assert lib.pico_comm_init(2, 2, uid, ctypes.byref(h)) == 1       # rank out of range
+    assert lib.pico_comm_init(1, 0, uid, None) == 1                  # NULL out
+    assert lib.pico_coreness_sharded(None, None, None, 4, 2, 0, 4, 0, None, None) == 1  # NULL comm
+    assert lib.pico_comm_size(None, None, None) == 1
+    assert lib.pico_comm_destroy(None) == 0

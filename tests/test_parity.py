@@ -218,3 +218,15 @@ def test_c1_pull_always_passes():
     for fl in (pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
                pico.F_PULL_ALWAYS | pico.F_TINY_TILES | pico.F_HOST_LOOP):
         _check(rp, ci, "histocore", fl, ref, jac)
+
+
+def test_auto_algorithm():
+    """PICO_ALGO_AUTO resolves by the degree skew and
+    size -- HistoCore on the skewed C1, PeelOne on a flat ER graph -- and
+    stays bit-exact; stats.algo reports the choice."""
+    for (rp, ci), want in ((synth.to_numpy(*synth.CONFIGS["C1"].build()), 0),
+                           (synth.to_numpy(*synth.erdos_renyi(400, 0.05, seed=77)), 1)):
+        ref = oracle.bz(rp, ci)
+        core, st, _ = _run(rp, ci, "auto")
+        assert st.algo == want
+        assert np.array_equal(core, ref)

@@ -9,6 +9,7 @@ vertices, whose changed sets are exactly HistoCore's C_t.
 GPU: the real shard kernels (include/pico_shard.h) in loopback mode -- P
 logical shards on one GPU, exchange = device concatenation -- against the
 oracle (coreness bit-exact, l2 and every |C_t| equal to the Jacobi sweeps)."""
+import ctypes
 import os
 import socket
 
@@ -201,3 +202,39 @@ def test_loopback_c1():
         core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
                                                         torch.from_numpy(ci).to(dev), parts)
         assert np.array_equal(core.cpu().numpy(), ref) and rounds == l2 and sizes == fs
+
+
+# ------------------------------------------------ one-call NCCL path (C ABI)
+@pytest.mark.gpu
+def test_sharded_abi_single_rank_nccl():
+    """pico_coreness_sharded_ex with the exchange inside libpico over NCCL, one
+    rank: bit-exact coreness and the Jacobi |F_t| sequence; argument checks."""
+    import torch
+    import oracle
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import sharded
+    dev = torch.device("cuda:0")
+    rp_np, ci_np = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    ref = oracle.bz(rp_np, ci_np)
+    _, l2, sizes = oracle.jacobi_rounds(rp_np, ci_np)
+    rp, ci = torch.from_numpy(rp_np).to(dev), torch.from_numpy(ci_np).to(dev)
+    n, m = rp.numel() - 1, ci.numel() // 2
+    comm = sharded.NcclComm(nranks=1, rank=0)
+    try:
+        for fl in (0, pico.F_TINY_TILES):
+            run = sharded.coreness_sharded_nccl(rp, ci, n, m, 0, comm, flags=fl)
+            torch.cuda.synchronize()
+            assert np.array_equal(run.core_local.cpu().numpy(), ref)
+            assert run.rounds == l2 and run.frontier_sizes == sizes
+        lib = pico.load()
+        out = torch.empty(n, dtype=torch.int32, device=dev)
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        # ranges must tile [0, n_global); arcs must sum to 2m; PeelOne is not sharded
+        assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n + 5, m, 0, n, 0,
+                                         out.data_ptr(), s) == 1
+        assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n, m + 1, 0, n, 0,
+                                         out.data_ptr(), s) == 1
+        assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n, m, 0, n, 1,
+                                         out.data_ptr(), s) == 2
+    finally:
+        comm.close()
