@@ -81,6 +81,9 @@ constexpr int kMaxPass = 8;
 #ifndef PICO_CBINS
 #define PICO_CBINS 16384
 #endif
+#ifndef PICO_ROUNDS_MINB
+#define PICO_ROUNDS_MINB 2         // resident 512-thread CTAs per SM of the round kernel
+#endif
 #ifndef PICO_PULL_AGG
 #define PICO_PULL_AGG 0            // warp-aggregate duplicate bin moves in pull mode
 #endif                             // (__match_any_sync; measured 1.4-3x slower)
@@ -918,8 +921,29 @@ __device__ void update_phase(const HcArgs &a, int t) {
 #ifndef PICO_PULL_U
 #define PICO_PULL_U 4
 #endif
-template <bool STATS>
-__device__ void coo_pull_phase(const HcArgs &a, int t) {
+// v-side estimate records: one GPU gathers the 4-byte records of its own
+// vertices (16|16 bits, saturated values fall back to the full arrays);
+// a shard gathers 8-byte records (32|32 bits, never saturated) of the
+// GLOBAL vertex space, fed by the exchanged triples (VRec64)
+struct VRec32 {
+    typedef unsigned T;
+    static constexpr int SH = 16;
+    static constexpr unsigned long long MASK = 0xffffull;
+    static constexpr bool SAT = true;
+};
+struct VRec64 {
+    typedef unsigned long long T;
+    static constexpr int SH = 32;
+    static constexpr unsigned long long MASK = 0xffffffffull;
+    static constexpr bool SAT = false;
+};
+
+__device__ __forceinline__ unsigned long long pack_rec64(int k, int old) {
+    return (unsigned long long)(unsigned)k | ((unsigned long long)(unsigned)old << 32);
+}
+
+template <bool STATS, class VR = VRec32>
+__device__ void coo_pull_phase(const HcArgs &a, int t, const typename VR::T *vrec) {
     constexpr int UA = PICO_PULL_U;
     const int lane = lane_id();
     const unsigned *chg = a.chg + (t & 1) * a.nwords;
@@ -939,7 +963,8 @@ __device__ void coo_pull_phase(const HcArgs &a, int t) {
     for (long long st = s0; st < s1; st++) {
         const long long e0 = bb + st * (32 * UA);
         int u[UA], v[UA];
-        unsigned ru[UA], rv[UA];
+        unsigned ru[UA];
+        typename VR::T rv[UA];
         long long hb[UA];
 #pragma unroll
         for (int q = 0; q < UA; q++) {
@@ -951,7 +976,7 @@ __device__ void coo_pull_phase(const HcArgs &a, int t) {
 #pragma unroll
         for (int q = 0; q < UA; q++) {
             ru[q] = u[q] >= 0 ? ld_rec(a.rec + u[q], hot) : 0u;
-            rv[q] = u[q] >= 0 ? ld_rec(a.rec + v[q], hot) : 0u;
+            rv[q] = u[q] >= 0 ? __ldcg(vrec + v[q]) : 0;
             hb[q] = u[q] >= 0 ? __ldg(a.rp + u[q]) - 1 : 0;
         }
 #pragma unroll
@@ -960,14 +985,14 @@ __device__ void coo_pull_phase(const HcArgs &a, int t) {
             if (STATS) st_arcs += ok;
             int cu = (int)(ru[q] & 0xffffu);
             if (ok && cu == (int)RSAT) cu = __ldcg(a.core + u[q]);
-            int nlo = (int)(rv[q] & 0xffffu), nhi = (int)(rv[q] >> 16);
+            int nlo = (int)(rv[q] & VR::MASK), nhi = (int)(rv[q] >> VR::SH);
             int cv = nlo, ov = nhi;
             bool ch = nlo != nhi;  // exact while the new half is unsaturated
-            if (ok && nlo == (int)RSAT) {  // estimate >= 65535: full arrays
+            if (VR::SAT && ok && nlo == (int)RSAT) {  // estimate >= 65535: full arrays
                 ch = (__ldcg(chg + (v[q] >> 5)) >> (v[q] & 31)) & 1u;
                 cv = __ldcg(a.core + v[q]);
                 ov = ch ? __ldcg(a.oldc + v[q]) : cv;
-            } else if (ok && ch && nhi == (int)RSAT && cu > (int)RSAT) {
+            } else if (VR::SAT && ok && ch && nhi == (int)RSAT && cu > (int)RSAT) {
                 ov = __ldcg(a.oldc + v[q]);  // saturated old half, needed exactly
             }
             bool g = ok && ch && cv < cu;  // N1/N3 neighbour
@@ -1157,7 +1182,7 @@ __device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool lea
 //   UpdateHisto(t)  |barrier|  SumHisto(t+1) over the marked vertices  |barrier|
 // ---------------------------------------------------------------------------
 template <bool STATS>
-__global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
+__global__ void __launch_bounds__(512, PICO_ROUNDS_MINB) hc_rounds_kernel(HcArgs a) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
@@ -1167,7 +1192,7 @@ __global__ void __launch_bounds__(512, 2) hc_rounds_kernel(HcArgs a) {
         bool pull = update_prologue(a, t, leader, gthread, nthreads, STATS);
         if (pull) {
             if (STATS && leader) a.ctl->st_pull++;
-            coo_pull_phase<STATS>(a, t);
+            coo_pull_phase<STATS>(a, t, a.rec);
         } else {
             update_phase<STATS>(a, t);
         }
@@ -1199,7 +1224,7 @@ __global__ void __launch_bounds__(512, 2) hc_update_kernel(HcArgs a, int t, int 
     update_prologue(a, t, leader, gthread, nthreads, STATS);
     if (pull) {
         if (STATS && leader) a.ctl->st_pull++;
-        coo_pull_phase<STATS>(a, t);
+        coo_pull_phase<STATS>(a, t, a.rec);
     } else {
         update_phase<STATS>(a, t);
     }
@@ -1246,20 +1271,21 @@ static bool hc_allow_pull(long long n, uint32_t flags) {
 
 // v-range width of a pull pass: 2^shift vertices whose 4-byte records fit
 // PICO_PASS_MB (the L2 slice one pass gathers from), at most kMaxPass passes
-static int hc_pshift(long long n, uint32_t flags) {
+// (rb: bytes per v-side record -- 4 on one GPU, 8 on a shard)
+static int hc_pshift(long long n, uint32_t flags, int rb = 4) {
     int sh = 0;
     if (flags & PICO_F_TINY_TILES) {  // exercise the passes on small graphs
         while ((1ll << sh) * 3 < n) sh++;
     } else {
-        while ((4ll << (sh + 1)) <= ((long long)PICO_PASS_MB << 20)) sh++;
+        while (((long long)rb << (sh + 1)) <= ((long long)PICO_PASS_MB << 20)) sh++;
     }
     while (((n - 1) >> sh) + 1 > kMaxPass) sh++;
     return sh;
 }
 
-static int hc_npass(long long n, uint32_t flags) {
+static int hc_npass(long long n, uint32_t flags, int rb = 4) {
     if (!hc_allow_pull(n, flags) || n < 2) return 1;
-    return (int)(((n - 1) >> hc_pshift(n, flags)) + 1);
+    return (int)(((n - 1) >> hc_pshift(n, flags, rb)) + 1);
 }
 
 struct HcLayout {
@@ -1270,10 +1296,14 @@ struct HcLayout {
     int npass;
 };
 
-static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
+// nv: size of the v-side id space (n on one GPU, n_global on a shard), rb:
+// bytes per v-side record
+static HcLayout hc_layout(long long n, long long arcs, uint32_t flags, long long nv = -1, int rb = 4) {
     Tune tn = hc_tune(flags);
     HcLayout L;
-    L.npass = hc_npass(n, flags);
+    if (nv < 0) nv = n;
+    const bool pull = hc_allow_pull(nv, flags);
+    L.npass = hc_npass(nv, flags, rb);
     L.nwords = (n + 31) / 32;
     L.scap = n + arcs / tn.seg + 64;
     L.hcap = 2 * (arcs / tn.seg) + 64;
@@ -1296,12 +1326,12 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags) {
     L.db = b; b += align256((size_t)n);
     L.slen = b; b += align256(sizeof(int) * (size_t)n);
     L.capd = b; b += align256(sizeof(unsigned) * (size_t)L.nwords);
-    const size_t el = hc_allow_pull(n, flags) ? (size_t)std::max(arcs, 1ll) : 1;  // pull edge list
+    const size_t el = pull ? (size_t)std::max(arcs, 1ll) : 1;  // pull edge list
     L.bk = b; b += align256(sizeof(unsigned long long) * (kMaxPass + 1));
     L.psrc = b; b += align256(sizeof(int) * el);
     L.pdst = b; b += align256(sizeof(int) * (L.npass > 1 ? el : 1));  // one bucket: colidx itself
     // edge-list build: bucket-major count matrix over the 2048-arc chunks + scan temp
-    L.nbcap = (hc_allow_pull(n, flags) && L.npass > 1) ? (arcs + kElChunk - 1) / kElChunk : 0;
+    L.nbcap = (pull && L.npass > 1) ? (arcs + kElChunk - 1) / kElChunk : 0;
     long long ncnt = std::max(1ll, L.npass * L.nbcap);
     L.elc = b; b += align256(sizeof(unsigned long long) * (size_t)ncnt);
     L.eltb = 0;
@@ -1607,28 +1637,53 @@ cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long ar
 // ===========================================================================
 struct Shard {
     HcArgs a;
+    HcLayout L;              // the rank's HcArgs arrays (rows: nloc; pull v-side: ng)
     void *ws;
     long long nloc, vb, ng, arcs;
     uint32_t flags;
     cudaStream_t s;
     DevInfo dev;
+    bool pull_ok;            // dense rounds may pull (graph size, flags)
     shadow_t *deg8g;         // [ng]   saturated global degrees (init)
     unsigned short *deg16g;  // [ng]
+    unsigned long long *grec;  // [ng] global estimate records new32 | old32 << 32 (pull rounds)
     long long *csc_off;      // [ng+1]
-    long long *csc_cur;      // [ng]
-    int *csc_idx;            // [arcs] owned neighbour (local id)
+    int *csc_idx;            // [arcs] owned neighbour (local id), grouped by v
+    int *tmpk;               // [arcs] sort keys out (CSC build)
     int2 *TS;                // (triple, segment) work items
     long long tscap;
-    unsigned long long *cnt; // [4] device counters
-    void *cubtmp;
+    unsigned long long *cnt; // [8] device counters: 0 pack, 1 nTS, 2 local arcs of C_t, 3 pull gate
+    void *cubtmp;            // scan / sort temp
     size_t cubbytes;
     int t;
 };
 
-__global__ void sh_deg8_kernel(const int *deg, long long ng, shadow_t *d8, unsigned short *d16) {
+// global degree shadows; every global record starts at (deg, deg) -- the
+// round-0 estimate, unchanged until a triple says otherwise
+__global__ void sh_deg8_kernel(const int *deg, long long ng, shadow_t *d8, unsigned short *d16,
+                               unsigned long long *grec) {
     long long nt = (long long)gridDim.x * blockDim.x;
-    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < ng; v += nt)
-        d8[v] = (shadow_t)min(deg[v], (int)SAT8), d16[v] = (unsigned short)min(deg[v], 65535);
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < ng; v += nt) {
+        int d = deg[v];
+        d8[v] = (shadow_t)min(d, (int)SAT8);
+        d16[v] = (unsigned short)min(d, 65535);
+        if (grec) grec[v] = pack_rec64(d, d);
+    }
+}
+
+// records of the received triples: (new, old) for the round's pull, then
+// (new, new) once the round is applied
+template <bool RESET>
+__global__ void sh_records_kernel(const int *tr, long long total, unsigned long long *grec) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += nt)
+        grec[tr[3 * i]] = pack_rec64(tr[3 * i + 2], RESET ? tr[3 * i + 2] : tr[3 * i + 1]);
+}
+
+// pull iff allowed and the received triples touch >= arcs_local / pull_div local arcs
+__global__ void sh_gate_kernel(unsigned long long *cnt, long long arcs, int pull_ok, int pull_div) {
+    if (threadIdx.x == 0)
+        cnt[3] = (pull_ok && cnt[2] * (unsigned long long)pull_div >= (unsigned long long)arcs) ? 1ull : 0ull;
 }
 
 // CSC counts per global vertex (into csc_off[v+1]) and scatter
@@ -1638,16 +1693,6 @@ __global__ void sh_csc_count_kernel(const int *ci, long long arcs, unsigned long
         atomicAdd(cnt_v + ci[e], 1ull);
 }
 
-__global__ void sh_csc_fill_kernel(const long long *rp, const int *ci, long long nloc, long long *cur,
-                                   int *idx) {
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long u = gw; u < nloc; u += nw)
-        for (long long e = rp[u] + lane_id(); e < rp[u + 1]; e += 32) {
-            unsigned long long pos = atomicAdd((unsigned long long *)(cur + ci[e]), 1ull);
-            idx[pos] = (int)u;
-        }
-}
 
 // C_t of this rank = segment-0 entries of S (init and SumHisto append one
 // (v, 0) per changed v) -> triples (v + vb, oldcore, core)
@@ -1680,29 +1725,35 @@ __global__ void sh_pack_kernel(HcArgs a, const unsigned long long *ns_dev, long 
     }
 }
 
-// (triple, segment) items for the CSC lists of the received triples
+// (triple, segment) items for the CSC lists of the received triples; the
+// local arcs they touch are summed into *arcs_ct (the pull decision)
 __global__ void sh_segments_kernel(const int *tr, long long total, const long long *csc_off, int seg, int2 *TS,
-                                   unsigned long long *nTS) {
+                                   unsigned long long *nTS, unsigned long long *arcs_ct) {
     long long nt = (long long)gridDim.x * blockDim.x;
     long long iters = (total + nt - 1) / nt;
+    long long ac = 0;
     for (long long it = 0; it < iters; it++) {
         long long i = it * nt + (long long)blockIdx.x * blockDim.x + threadIdx.x;
         int ns = 0;
         if (i < total) {
             int v = tr[3 * i];
-            ns = nseg_of(csc_off[v + 1] - csc_off[v], seg);
+            long long len = csc_off[v + 1] - csc_off[v];
+            ac += len;
+            ns = nseg_of(len, seg);
         }
         warp_append_segments((int)i, ns, TS, nTS);
     }
+    stat_add(arcs_ct, ac);
 }
 
 // UpdateHisto of the received triples over the local CSC (push direction)
 __global__ void __launch_bounds__(512, 2) sh_update_kernel(HcArgs a, const int *tr, const int2 *TS,
                                                            const unsigned long long *nts_dev,
                                                            const long long *csc_off, const int *csc_idx,
-                                                           unsigned long long *nF) {
+                                                           unsigned long long *nF, const unsigned long long *gate) {
     constexpr int U = 4;
     const int lane = lane_id();
+    if (bcast_u64(gate)) return;  // this round pulls
     const long long nts = (long long)bcast_u64(nts_dev);  // no host round trip
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -1757,20 +1808,48 @@ __global__ void __launch_bounds__(512, 2) sh_update_kernel(HcArgs a, const int *
     }
 }
 
+// the other kernels of a shard round, gated by the pull decision (uniform)
+__global__ void __launch_bounds__(512, 2) sh_pull_kernel(HcArgs a, int t, const unsigned long long *grec,
+                                                         const unsigned long long *gate) {
+    if (!bcast_u64(gate)) return;
+    coo_pull_phase<false, VRec64>(a, t, grec);
+}
+
+__global__ void __launch_bounds__(512, 2) sh_collect_kernel(HcArgs a, int t, const unsigned long long *gate) {
+    if (!bcast_u64(gate)) return;
+    collect_sum_phase<false>(a, t);
+}
+
+__global__ void __launch_bounds__(512) sh_sum_kernel(HcArgs a, int t, const unsigned long long *gate) {
+    if (bcast_u64(gate)) return;
+    const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    sum_phase<false>(a, t, gthread, nthreads);
+}
+
+static size_t sort_bytes(long long arcs) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs((void *)nullptr, b, (const int *)nullptr, (int *)nullptr, (const int *)nullptr,
+                                    (int *)nullptr, (int)std::max(arcs, 1ll));
+    return b;
+}
+
 size_t shard_workspace_bytes(long long nloc, long long ng, long long arcs, uint32_t flags, long long *tscap,
                              size_t *cubbytes) {
     Tune tn = hc_tune(flags);
-    size_t b = align256(hc_layout(nloc, arcs, flags).total);
+    size_t b = align256(hc_layout(nloc, arcs, flags, ng, 8).total);
     b += align256(sizeof(shadow_t) * (size_t)ng);
     b += align256(sizeof(unsigned short) * (size_t)ng);
-    b += align256(sizeof(long long) * (size_t)(ng + 1)) * 2;
-    b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
+    b += align256(sizeof(unsigned long long) * (size_t)ng);       // grec
+    b += align256(sizeof(long long) * (size_t)(ng + 1)) * 2;      // csc_off (+ counts)
+    b += align256(sizeof(int) * (size_t)std::max(arcs, 1ll)) * 2; // csc_idx, tmpk
     *tscap = ng + arcs / tn.seg + 64;
     b += align256(sizeof(int2) * (size_t)*tscap);
-    b += align256(sizeof(unsigned long long) * 4);
+    b += align256(sizeof(unsigned long long) * 8);
     b += align256(sizeof(int) * (size_t)std::max(nloc, 1ll));  // local core
     size_t cb = 0;
     cub::DeviceScan::ExclusiveSum((void *)nullptr, cb, (const long long *)nullptr, (long long *)nullptr, (int)(ng + 1));
+    cb = std::max(cb, sort_bytes(arcs));
     *cubbytes = cb;
     b += align256(cb);
     return b;
@@ -1783,9 +1862,12 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     cudaError_t e = cudaMemcpyAsync(&h->arcs, rp + nloc, sizeof(long long), cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     if (e) { delete h; return e; }
+    if (h->arcs > INT_MAX) { delete h; return cudaErrorNotSupported; }  // 32-bit sort / scan counts
     size_t bytes = shard_workspace_bytes(nloc, ng, h->arcs, flags, &h->tscap, &h->cubbytes);
     if ((e = cudaMallocAsync(&h->ws, bytes, s))) { delete h; return e; }
-    HcLayout L = hc_layout(nloc, h->arcs, flags);
+    HcLayout L = hc_layout(nloc, h->arcs, flags, ng, 8);
+    h->L = L;
+    h->pull_ok = hc_allow_pull(ng, flags) && h->arcs > 0;
     char *p = (char *)h->ws;
     HcArgs &a = h->a;
     a.ctl = (Ctrl *)(p + L.ctl);
@@ -1809,26 +1891,32 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.capd = (unsigned *)(p + L.capd);
     a.nwords = L.nwords;
     a.rp = rp; a.ci = ci; a.n = (int)nloc; a.arcs = h->arcs; a.tn = hc_tune(flags);
-    a.allow_pull = 0;
-    a.npass = 1;
-    a.pshift = 30;
-    a.boff = nullptr;
-    a.psrc = a.pdst = nullptr;
-    a.prefilter = 0;  // the shard's UpdateHisto walks the CSC, not the rows
+    a.allow_pull = 0;  // (the single-GPU round kernel's switch; shards gate per round)
+    // pull rounds: the local arcs (u local, v global) bucketed by global v-range
+    a.boff = (unsigned long long *)(p + L.bk);
+    a.psrc = (int *)(p + L.psrc);
+    a.pdst = (int *)(p + L.pdst);
+    a.npass = L.npass;
+    a.pshift = hc_pshift(ng, flags, 8);
+    if (L.npass == 1) a.pdst = const_cast<int *>(ci);
+    a.prefilter = 0;  // the shard's push UpdateHisto walks the CSC, not the rows
     p += align256(L.total);
     h->deg8g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
     h->deg16g = (unsigned short *)p; p += align256(sizeof(unsigned short) * (size_t)ng);
-    h->csc_off = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
-    h->csc_cur = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1));
+    h->grec = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * (size_t)ng);
+    h->csc_off = (long long *)p; p += align256(sizeof(long long) * (size_t)(ng + 1)) * 2;
     h->csc_idx = (int *)p; p += align256(sizeof(int) * (size_t)std::max(h->arcs, 1ll));
+    h->tmpk = (int *)p; p += align256(sizeof(int) * (size_t)std::max(h->arcs, 1ll));
     h->TS = (int2 *)p; p += align256(sizeof(int2) * (size_t)h->tscap);
-    h->cnt = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * 4);
+    h->cnt = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * 8);
     a.core = (int *)p; p += align256(sizeof(int) * (size_t)std::max(nloc, 1ll));
     h->cubtmp = p;
     Ctrl hc{};
     hc.mincv[0] = hc.mincv[1] = INT_MAX;
     if (!e) e = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)L.nwords, s);
+    if (!e) e = cudaMemsetAsync(a.capd, 0, sizeof(unsigned) * (size_t)L.nwords, s);
+    if (!e) e = cudaMemsetAsync(h->cnt, 0, sizeof(unsigned long long) * 8, s);
     // H0 on the owned rows: core = oldcore = deg, shadow, degree classes
     int blocks = (int)std::min<long long>((nloc + 255) / 256, (long long)dev.sms * 16);
     if (!e && nloc > 0) {
@@ -1850,28 +1938,56 @@ cudaError_t shard_degrees(Shard *h, int *deg_out) {
 }
 
 // InitHisto + round-1 SumHisto of the owned rows (neighbour degrees from the
-// all-gathered deg_global) and the local CSC
+// all-gathered deg_global), the local CSC (the transpose of the owned rows:
+// for every global v its owned neighbours, by a key-value radix sort of the
+// arcs) and, if dense rounds may pull, the bucketed local edge list
 cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
     cudaStream_t s = h->s;
     HcArgs &a = h->a;
+    const HcLayout &L = h->L;
     const int sms = h->dev.sms;
     auto grid = [&](long long work) {
         return std::max(1, (int)std::min<long long>((work + 255) / 256, (long long)sms * 16));
     };
     cudaError_t e;
-    sh_deg8_kernel<<<grid(h->ng), 256, 0, s>>>(deg_global, h->ng, h->deg8g, h->deg16g);
+    sh_deg8_kernel<<<grid(h->ng), 256, 0, s>>>(deg_global, h->ng, h->deg8g, h->deg16g, h->pull_ok ? h->grec : nullptr);
     a.nv8 = h->deg8g;
     a.nv16 = h->deg16g;
     a.nv32 = deg_global;
-    // CSC: counts -> exclusive scan -> scatter
-    if ((e = cudaMemsetAsync(h->csc_cur, 0, sizeof(long long) * (size_t)(h->ng + 1), s))) return e;
-    if (h->arcs)
-        sh_csc_count_kernel<<<grid(h->arcs), 256, 0, s>>>(a.ci, h->arcs, (unsigned long long *)h->csc_cur);
-    size_t cb = h->cubbytes;
-    if ((e = cub::DeviceScan::ExclusiveSum(h->cubtmp, cb, h->csc_cur, h->csc_off, (int)(h->ng + 1), s))) return e;
-    if ((e = cudaMemcpyAsync(h->csc_cur, h->csc_off, sizeof(long long) * (size_t)h->ng, cudaMemcpyDeviceToDevice, s)))
-        return e;
-    if (h->nloc) sh_csc_fill_kernel<<<sms * 8, 256, 0, s>>>(a.rp, a.ci, h->nloc, h->csc_cur, h->csc_idx);
+    if (h->arcs > 0) {
+        // row owner of every local arc (into psrc for one bucket, else the
+        // not-yet-written histogram space)
+        int *src = (h->pull_ok && L.npass == 1) ? a.psrc : a.histo;
+        hc_el_src_short_kernel<<<grid(h->nloc), 256, 0, s>>>(a, src);
+        hc_el_src_long_kernel<<<sms * 8, 256, 0, s>>>(a, src);
+        if (h->pull_ok && L.npass > 1) {
+            unsigned long long *cnt = (unsigned long long *)((char *)h->ws + L.elc);
+            hc_el_count_kernel<<<sms * 16, 256, 0, s>>>(a, cnt, L.nbcap);
+            size_t tb = L.eltb;
+            if ((e = cub::DeviceScan::ExclusiveSum((char *)h->ws + L.elt, tb, cnt, cnt, (int)(L.npass * L.nbcap), s)))
+                return e;
+            hc_el_fill_kernel<<<sms * 16, 256, 0, s>>>(a, src, cnt, L.nbcap);
+            hc_el_offsets_kernel<<<1, 32, 0, s>>>(a, L.nbcap, cnt);
+        } else if (h->pull_ok) {
+            unsigned long long off[kMaxPass + 1];
+            for (int q = 0; q <= kMaxPass; q++) off[q] = q == 0 ? 0 : (unsigned long long)h->arcs;
+            if ((e = cudaMemcpyAsync(a.boff, off, sizeof(off), cudaMemcpyHostToDevice, s))) return e;
+        }
+        // CSC: counts -> offsets; (v, u) pairs sorted by v -> owned neighbours
+        long long *cntv = h->csc_off + (h->ng + 1);
+        if ((e = cudaMemsetAsync(cntv, 0, sizeof(long long) * (size_t)(h->ng + 1), s))) return e;
+        sh_csc_count_kernel<<<grid(h->arcs), 256, 0, s>>>(a.ci, h->arcs, (unsigned long long *)cntv);
+        size_t cb = h->cubbytes;
+        if ((e = cub::DeviceScan::ExclusiveSum(h->cubtmp, cb, cntv, h->csc_off, (int)(h->ng + 1), s))) return e;
+        int bits = 1;
+        while ((1ll << bits) < h->ng) bits++;
+        cb = h->cubbytes;
+        if ((e = cub::DeviceRadixSort::SortPairs(h->cubtmp, cb, a.ci, h->tmpk, src, h->csc_idx, (int)h->arcs, 0,
+                                                 bits, s)))
+            return e;
+    } else {
+        if ((e = cudaMemsetAsync(h->csc_off, 0, sizeof(long long) * (size_t)(h->ng + 1), s))) return e;
+    }
     // InitHisto fused with round-1 SumHisto (the single-GPU init kernels)
     if (h->nloc) {
         Tune tn = a.tn;
@@ -1913,27 +2029,43 @@ cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count) 
     return cudaGetLastError();
 }
 
-// UpdateHisto(C_t of all ranks) over the local CSC, then SumHisto(F_{t+1})
+// UpdateHisto(C_t of all ranks) -- push over the local CSC, or, for dense
+// rounds, pull over the bucketed local edge list against the global records
+// -- then SumHisto of the local frontier.  The direction is decided on the
+// device (sh_gate_kernel): no host round trip.
 cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed) {
     cudaStream_t s = h->s;
     HcArgs &a = h->a;
     const int sms = h->dev.sms;
     const int t = h->t;
     cudaError_t e;
-    unsigned long long *nTS = h->cnt + 1;
-    if ((e = cudaMemsetAsync(nTS, 0, sizeof(unsigned long long), s))) return e;
+    unsigned long long *nTS = h->cnt + 1, *gate = h->cnt + 3;
+    if ((e = cudaMemsetAsync(h->cnt + 1, 0, sizeof(unsigned long long) * 3, s))) return e;  // nTS, arcs, gate
     if ((e = cudaMemsetAsync(&a.ctl->nF[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
     if ((e = cudaMemsetAsync(&a.ctl->nS[(t + 1) & 1], 0, sizeof(unsigned long long), s))) return e;
+    if ((e = cudaMemsetAsync(a.chg + ((t + 1) & 1) * a.nwords, 0, sizeof(unsigned) * (size_t)a.nwords, s))) return e;
     // stream-ordered, no host round trip: work counts are read on the device
     // (the segment capacity n_global + 2m_local/seg bounds any round: the
     // triples are distinct vertices)
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh_pull_kernel, 512, 0);
+    const int pblocks = sms * std::max(1, occ);
     if (total > 0) {
         int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-        sh_segments_kernel<<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->csc_off, a.tn.seg, h->TS, nTS);
+        if (h->pull_ok) sh_records_kernel<false><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec);
+        sh_segments_kernel<<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->csc_off, a.tn.seg, h->TS, nTS,
+                                                               h->cnt + 2);
+        sh_gate_kernel<<<1, 32, 0, s>>>(h->cnt, h->arcs, h->pull_ok ? 1 : 0, a.tn.pull_div);
         sh_update_kernel<<<sms * 2, 512, 0, s>>>(a, triples, h->TS, nTS, h->csc_off, h->csc_idx,
-                                                 &a.ctl->nF[(t + 1) & 1]);
+                                                 &a.ctl->nF[(t + 1) & 1], gate);
+        if (h->pull_ok) sh_pull_kernel<<<pblocks, 512, 0, s>>>(a, t, h->grec, gate);
     }
-    hc_sum_kernel<false><<<sms * 4, 512, 0, s>>>(a, t + 1);
+    sh_sum_kernel<<<sms * 4, 512, 0, s>>>(a, t + 1, gate);
+    if (h->pull_ok && total > 0) {
+        sh_collect_kernel<<<pblocks, 512, 0, s>>>(a, t + 1, gate);
+        int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+        sh_records_kernel<true><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec);
+    }
     if ((e = cudaGetLastError())) return e;
     h->t = t + 1;
     if (changed) {

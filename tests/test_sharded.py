@@ -184,7 +184,7 @@ def test_loopback_parity(parts):
     for name, (rp, ci) in _graphs():
         ref = oracle.bz(rp, ci)
         _, l2, fs = oracle.jacobi_rounds(rp, ci)
-        for fl in (0, pico.F_TINY_TILES):
+        for fl in (0, pico.F_TINY_TILES, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES):
             core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
                                                             torch.from_numpy(ci).to(dev), parts, fl)
             got = core.cpu().numpy()
@@ -198,10 +198,12 @@ def test_loopback_c1():
     dev = torch.device("cuda:0")
     ref = oracle.bz(rp, ci)
     _, l2, fs = oracle.jacobi_rounds(rp, ci)
+    import paper_2402_15253_b200 as pico
     for parts in (2, 8):
-        core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
-                                                        torch.from_numpy(ci).to(dev), parts)
-        assert np.array_equal(core.cpu().numpy(), ref) and rounds == l2 and sizes == fs
+        for fl in (0, pico.F_PULL_ALWAYS):  # push rounds over the CSC / pull rounds over the edge list
+            core, rounds, sizes = sharded.coreness_loopback(torch.from_numpy(rp).to(dev),
+                                                            torch.from_numpy(ci).to(dev), parts, fl)
+            assert np.array_equal(core.cpu().numpy(), ref) and rounds == l2 and sizes == fs
 
 
 # ------------------------------------------------ one-call NCCL path (C ABI)
@@ -221,7 +223,7 @@ def test_sharded_abi_single_rank_nccl():
     n, m = rp.numel() - 1, ci.numel() // 2
     comm = sharded.NcclComm(nranks=1, rank=0)
     try:
-        for fl in (0, pico.F_TINY_TILES):
+        for fl in (0, pico.F_TINY_TILES, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES):
             run = sharded.coreness_sharded_nccl(rp, ci, n, m, 0, comm, flags=fl)
             torch.cuda.synchronize()
             assert np.array_equal(run.core_local.cpu().numpy(), ref)
