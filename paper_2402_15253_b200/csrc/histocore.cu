@@ -843,15 +843,19 @@ template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
     const int lane = lane_id();
     const long long ns = (long long)bcast_u64(&a.ctl->nS[t & 1]);
-    const long long nbatch = (ns + 31) >> 5;
     unsigned long long *wc = &a.ctl->wc[t & 1];
     long long st_arcs = 0, st_guard = 0;
     const unsigned long long hot = pol_last(), cold = pol_first();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    // segments per warp batch: 32 when there is work for every warp, fewer in
+    // small rounds so that they still spread over all warps (a warp walks its
+    // batch's arcs serially, 32*U at a time)
+    const int bs = (int)min(32ll, max(1ll, (ns + nwarps - 1) / nwarps));
+    const long long nbatch = (ns + bs - 1) / bs;
     for (long long round = 0;; round++) {
         // first batch static (warp id), the rest claimed dynamically (one
-        // atomic per 32 work items); small rounds cost no claim atomics
+        // atomic per batch); small rounds cost no claim atomics
         long long bidx = gwarp;
         if (round > 0) {
             if (nbatch <= nwarps) break;
@@ -859,10 +863,10 @@ __device__ void update_phase(const HcArgs &a, int t) {
             bidx = __shfl_sync(FULL, bidx, 0);
         }
         if (bidx >= nbatch) break;
-        long long i = bidx * 32 + lane;
+        long long i = bidx * bs + lane;
         long long b = 0;
         int len = 0, cv = 0, ov = 0;
-        if (i < ns) {
+        if (lane < bs && i < ns) {
             int2 sg = ld_stream_int2(a.S + i, cold);
             long long r0 = __ldg(a.rp + sg.x);
             long long r1 = r0 + __ldcg(a.slen + sg.x);  // (prefiltered) prefix of the row
