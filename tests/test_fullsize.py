@@ -1,0 +1,57 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (plain pico_coreness_ex calls on the device CSR): the whole coreness
+vector of every single-GPU config against the serial BZ oracle (SURVEY 8(c):
+the result is unique, so the comparison is element by element), plus the
+iteration counts the oracle pins cheaply at this size (k_max, PeelOne's
+non-empty levels = number of distinct nonzero coreness values) and the
+k-core definition check.  C2/C3 take seconds; T and C4 (2.1 G and 2.7 G arcs)
+about a minute each of serial BZ on one host core."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(cfg):
+    import torch
+    rp, ci = synth.CONFIGS[cfg].build(device=torch.device("cuda:0"))
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rp, ci
+
+
+def _check(cfg, kcore=True):
+    import torch
+    import paper_2402_15253_b200 as pico
+    rp, ci = _graph(cfg)
+    rp_np, ci_np = synth.to_numpy(rp, ci)
+    ref = oracle.bz(rp_np, ci_np)
+    nz = ref[ref > 0]
+    for algo in ("histocore", "peelone"):
+        st = pico.Stats()
+        core = pico.coreness(rp, ci, algo=algo, stats=st).cpu().numpy()
+        if not np.array_equal(core, ref):
+            bad = np.flatnonzero(core != ref)
+            raise AssertionError(f"{cfg} {algo}: {bad.size} mismatches, first v={bad[0]}: {core[bad[0]]} != {ref[bad[0]]}")
+        if algo == "peelone":
+            assert st.levels == np.unique(nz).size
+            assert st.kmax == int(nz.max())
+        else:
+            assert st.rounds > 0
+    if kcore:
+        assert oracle.kcore_check(rp_np, ci_np, ref)
+    del rp, ci
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_full_size_social(cfg):
+    _check(cfg)
+
+
+@pytest.mark.parametrize("cfg", ["T", "C4"])
+def test_full_size_billion_edges(cfg):
+    _check(cfg, kcore=False)
