@@ -66,6 +66,18 @@ def hc_bytes(n: int, m: int, st: dict, f1: int, relabelled: bool = False) -> dic
     return out
 
 
+def i2c_bytes(n: int, m: int, st: dict, relabelled: bool = False) -> dict:
+    """CntCore / NbrCore ablations, the same 4-byte
+    access model: every neighbour-list entry read costs its colidx word and
+    the neighbour's estimate (8 B; arcs_scanned counts them), every HINDEX
+    evaluation its core read and write (8 B), every active vertex its
+    rowptr pair (16 B)."""
+    out = {"rounds": 8 * st["arcs_scanned"] + 8 * st["frontier_total"] + 16 * st["alive_scanned"]}
+    if relabelled:
+        out["relabel"] = relabel_bytes(n, m)
+    return out
+
+
 def relabel_bytes(n: int, m: int) -> int:
     """Internal relabel: degree keys (rowptr 8(n+1), keys+ids 8n), radix sort of
     n (key, id) pairs (4 passes x 16 B), perm/rowptr2 (12n), row copy (rowptr
@@ -261,6 +273,10 @@ def bench_single(args):
 
     results = {}
     algos = [args.algo] + ([a for a in ("histocore", "peelone") if a != args.algo] if args.both else [])
+    # Index2core ablations (CntCore, NbrCore; the paper's Table tab:nbrcnthisto) on graphs where they
+    # finish in seconds
+    if args.ablations == "on" or (args.ablations == "auto" and 2 * m <= (320 << 20)):
+        algos += ["cntcore", "nbrcore"]
     core_ref = None
     for algo in algos:
         # untimed instrumented run: iteration counts + work counters for B_alg
@@ -299,8 +315,10 @@ def bench_single(args):
         rl = "relabel" in kms
         if algo == "histocore":
             byts = hc_bytes(n, m, sd, int(fs[0]) if sd["rounds"] > 0 else 0, rl)
-        else:
+        elif algo == "peelone":
             byts = po_bytes(n, m, sd, rl)
+        else:
+            byts = i2c_bytes(n, m, sd, rl)
         dom = max(kms, key=kms.get)
         ach = byts.get(dom, 0) / (kms[dom] * 1e-3) / 1e9
         total_b = sum(byts.values())
@@ -386,6 +404,8 @@ def main():
     ap.add_argument("--impl", default="pico", choices=["pico", "reference"])
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-both", dest="both", action="store_false")
+    ap.add_argument("--ablations", default="auto", choices=["auto", "on", "off"],
+                    help="also time CntCore / NbrCore (auto: graphs up to 320 M arcs)")
     ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
                     help="sharded path: NCCL inside libpico (pico_coreness_sharded) or torch.distributed")

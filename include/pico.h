@@ -60,10 +60,15 @@ typedef struct CUstream_st *pico_stream_t;
 typedef enum {
     PICO_ALGO_HISTOCORE = 0, /* Alg 6, P:489-539 (primary kernel)           */
     PICO_ALGO_PEELONE = 1,   /* Alg 4 + dynamic frontier       */
-    PICO_ALGO_AUTO = 2       /* pick one of the two from the degree skew  */
+    PICO_ALGO_AUTO = 2,      /* pick one of the two from the degree skew  */
                              /* d_max * n / 2m and the size 2m (SURVEY    */
                              /* 8(f) NEXT-2; rule and data: DESIGN.md);   */
                              /* stats->algo reports the choice            */
+    /* Index2core ablations, same coreness and rounds: */
+    PICO_ALGO_CNTCORE = 3,   /* Alg 5 CntCore: frontiers by cnt, */
+                             /* HINDEX rebuilt from all neighbours        */
+    PICO_ALGO_NBRCORE = 4    /* NbrCore: every neighbour of a     */
+                             /* changed vertex recomputes HINDEX          */
 } pico_algo_t;
 
 typedef enum {
@@ -131,15 +136,19 @@ typedef struct {
                             /* drained the dynamic frontiers of all levels   */
     int64_t kmax;           /* max coreness                                   */
     /* work counters (PICO_F_STATS), the terms of DESIGN.md "algorithmic bytes" */
-    int64_t frontier_total;     /* HistoCore: sum_t |F_t| incl. round 1        */
+    int64_t frontier_total;     /* HistoCore: sum_t |F_t| incl. round 1;       */
+                                /* Cnt/NbrCore: HINDEX evaluations             */
     int64_t init_slots_written; /* HistoCore: histogram slots written by init  */
     int64_t arcs_scanned;       /* HistoCore: sum_t S_t (UpdateHisto arcs);    */
+                                /* Cnt/NbrCore: neighbour entries read (the    */
+                                /* edge accesses of the paper's Fig 3);        */
                                 /* PeelOne: arcs of processed vertices          */
     int64_t guarded_arcs;       /* HistoCore: arcs with core[u] > core[v];     */
                                 /* PeelOne: clamped decrements issued            */
     int64_t bins_read;          /* HistoCore: SumHisto bins read (rounds >= 2) */
     int64_t pushes;             /* vertices pushed into a next frontier/queue  */
-    int64_t alive_scanned;      /* PeelOne: sum over levels of |alive list|    */
+    int64_t alive_scanned;      /* PeelOne: sum over levels of |alive list|;   */
+                                /* Cnt/NbrCore: sum over rounds of |V_active|  */
     int64_t hub_fallbacks;      /* vertices that needed the global-bin path    */
     int64_t segments;           /* HistoCore: UpdateHisto work items (v, seg)  */
                                 /* produced; PeelOne: queue entries processed  */

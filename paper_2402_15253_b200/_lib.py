@@ -10,7 +10,7 @@ import re
 
 from .build import INCLUDE, LIB
 
-ALGOS = {"histocore": 0, "peelone": 1, "auto": 2}
+ALGOS = {"histocore": 0, "peelone": 1, "auto": 2, "cntcore": 3, "nbrcore": 4}
 
 F_VALIDATE = 1
 F_STATS = 2

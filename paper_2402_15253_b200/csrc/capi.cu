@@ -172,6 +172,7 @@ static size_t algo_bytes(long long n, long long arcs, int algo, uint32_t flags) 
     if (algo == PICO_ALGO_PEELONE) return po_workspace_bytes(n, arcs, flags);
     if (algo == PICO_ALGO_AUTO)
         return std::max(hc_workspace_bytes(n, arcs, flags), po_workspace_bytes(n, arcs, flags));
+    if (algo == PICO_ALGO_CNTCORE || algo == PICO_ALGO_NBRCORE) return i2c_workspace_bytes(n, arcs);
     return 0;
 }
 
@@ -221,8 +222,7 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
     g_last_error.clear();
     reset_stats(stats);
     if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n (%lld) or m (%lld)", (long long)n, (long long)m);
-    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE && algo != PICO_ALGO_AUTO)
-        return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (algo < PICO_ALGO_HISTOCORE || algo > PICO_ALGO_NBRCORE) return fail(PICO_EINVAL, "unknown algo %d", algo);
     if (stats) stats->algo = algo == PICO_ALGO_AUTO ? PICO_ALGO_HISTOCORE : algo;
     if (n == 0) return PICO_OK;
     if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n = %lld needs 64-bit vertex ids", (long long)n);
@@ -302,9 +302,12 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
             if (rc == PICO_OK) {
                 if (algo == PICO_ALGO_HISTOCORE)
                     e = hc_run(grp, gci, gn, arcs, gcore, s, flags, aws, stats, dev);
-                else
+                else if (algo == PICO_ALGO_PEELONE)
                     e = po_run(grp, gci, gn, arcs, gcore, s, flags, aws, stats, dev);
-                if (e) rc = cuda_fail(e, algo == PICO_ALGO_HISTOCORE ? "histocore" : "peelone");
+                else
+                    e = i2c_run(grp, gci, gn, arcs, gcore, s, flags, algo == PICO_ALGO_CNTCORE, aws, stats, dev);
+                static const char *names[] = {"histocore", "peelone", "auto", "cntcore", "nbrcore"};
+                if (e) rc = cuda_fail(e, names[algo]);
             }
             if (rc == PICO_OK && relabel) {
                 cudaEvent_t b0 = nullptr, b1 = nullptr;
@@ -329,7 +332,7 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
             }
             if (r0) { cudaEventDestroy(r0); cudaEventDestroy(r1); }
             e = cudaSuccess;
-            if (!e && stats && algo == PICO_ALGO_HISTOCORE) {
+            if (!e && stats && algo != PICO_ALGO_PEELONE) {  // (PeelOne counts k_max itself)
                 int *d = (int *)ws;  // Ctrl region is free again
                 int km = 0;
                 e = cudaMemsetAsync(d, 0, sizeof(int), s);
@@ -362,8 +365,7 @@ int pico_coreness_host(const int64_t *rowptr_h, const int32_t *colidx_h, int64_t
     g_last_error.clear();
     reset_stats(stats);
     if (n < 0 || m < 0) return fail(PICO_EINVAL, "negative n or m");
-    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE && algo != PICO_ALGO_AUTO)
-        return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (algo < PICO_ALGO_HISTOCORE || algo > PICO_ALGO_NBRCORE) return fail(PICO_EINVAL, "unknown algo %d", algo);
     if (n == 0) return PICO_OK;
     if (!rowptr_h || !core_out_h || (m > 0 && !colidx_h)) return fail(PICO_EINVAL, "NULL pointer argument");
     if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n too large");

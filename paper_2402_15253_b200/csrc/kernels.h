@@ -22,6 +22,11 @@ size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags);
 cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);
 
+// CntCore / NbrCore ablations (index2core.cu); cnt_filter selects CntCore
+size_t i2c_workspace_bytes(long long n, long long arcs);
+cudaError_t i2c_run(const long long *rp, const int *ci, long long n, long long arcs, int *core, cudaStream_t s,
+                    uint32_t flags, bool cnt_filter, void *ws, pico_stats_t *st, const DevInfo &dev);
+
 size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags);
 cudaError_t po_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);

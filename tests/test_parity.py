@@ -230,3 +230,28 @@ def test_auto_algorithm():
         core, st, _ = _run(rp, ci, "auto")
         assert st.algo == want
         assert np.array_equal(core, ref)
+
+
+@pytest.mark.parametrize("algo", ["cntcore", "nbrcore"])
+def test_index2core_ablations(algo):
+    """CntCore (Alg 5) and NbrCore: the same coreness and
+    the same synchronous rounds (l2 and every |C_t|) as the Jacobi reference,
+    on the fixtures, the small corpus, rows in arbitrary order and C1."""
+    graphs = [g for _, g in _fixture_graphs()] + [g for _, g in corpus()]
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    ci2 = ci.copy()
+    rng = np.random.default_rng(3)
+    for v in range(rp.size - 1):
+        rng.shuffle(ci2[rp[v]:rp[v + 1]])
+    graphs += [(rp, ci2), synth.to_numpy(*synth.CONFIGS["C1"].build())]
+    for rp, ci in graphs:
+        ref = oracle.bz(rp, ci)
+        _, l2, sizes = oracle.jacobi_rounds(rp, ci)
+        core, st, fs = _run(rp, ci, algo, pico_flags_stats())
+        assert np.array_equal(core, ref)
+        assert st.rounds == l2 and list(fs[:l2]) == sizes
+        assert st.kmax == (int(ref.max()) if ref.size else 0)
+
+
+def pico_flags_stats():
+    return _pico().F_STATS
