@@ -1,0 +1,54 @@
+/*
+ * pico_dyn.h -- C ABI of decremental HistoCore in libpico.so (core
+ * maintenance under edge deletions).
+ *
+ * PAPER.md P:61 and P:882-884 name dynamic graphs as a setting the
+ * Index2core paradigm suits.  After a HistoCore run (Alg 6) every
+ * estimate equals the coreness and every per-vertex histogram is exact; a
+ * deletion can only lower coreness, so the current coreness is an upper bound
+ * of the new one and the same rounds, started from the histograms with the
+ * deleted neighbours taken out, converge to the new coreness without
+ * rebuilding anything.
+ *
+ * Conventions (beyond those of pico.h):
+ *  - pico_dyn_create copies the graph (device CSR, as pico_coreness) into a
+ *    handle-owned buffer and runs HistoCore; the caller's arrays are not
+ *    kept.  Internal compaction (PICO_F_RELABEL) does not apply.
+ *  - src / dst are DEVICE int32 arrays of k undirected edges {src[i], dst[i]}
+ *    that must be edges of the current graph, pairwise distinct; both arcs
+ *    are removed.  A missing edge, a self loop or an id out of range ->
+ *    PICO_EINVAL, after which the handle is unusable (destroy it).
+ *  - Calls are blocking and ordered on the stream given at creation.
+ *  - Insertions are not supported (they can raise coreness, which the
+ *    decreasing Index2core iteration cannot follow from the current state).
+ */
+#ifndef PICO_DYN_H_
+#define PICO_DYN_H_
+
+#include "pico.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pico_dyn_s *pico_dyn_t;
+
+/* Copy the graph, run HistoCore, keep its state.  flags: PICO_F_* schedule
+ * flags of pico.h; stats (optional) as in pico_coreness_ex for this run. */
+int pico_dyn_create(const int64_t *rowptr, const int32_t *colidx, int64_t n, int64_t m, uint32_t flags,
+                    pico_stream_t stream, pico_stats_t *stats, pico_dyn_t *out);
+
+/* core_out (device int32 [n]) <- the coreness of the current graph. */
+int pico_dyn_coreness(pico_dyn_t h, int32_t *core_out);
+
+/* Delete k undirected edges and bring the coreness up to date.  stats
+ * (optional): rounds of the update and, with frontier_sizes set, |C_t| of
+ * each. */
+int pico_dyn_delete_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, int64_t k, pico_stats_t *stats);
+
+int pico_dyn_destroy(pico_dyn_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PICO_DYN_H_ */

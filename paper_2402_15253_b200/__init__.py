@@ -18,7 +18,7 @@ import numpy as np
 from ._lib import (ALGOS, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
                    F_RELABEL, F_STATS, F_TIMING, F_TINY_TILES, F_VALIDATE, PicoError, Stats, check, header_functions, load)
 
-__all__ = ["coreness", "coreness_host", "workspace_bytes", "PicoError", "Stats", "load",
+__all__ = ["coreness", "coreness_host", "workspace_bytes", "DynamicCoreness", "PicoError", "Stats", "load",
            "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES",
            "F_PUSH_ONLY", "F_PULL_ALWAYS", "F_RELABEL", "F_NO_RELABEL", "F_CLAMP_CAS", "F_PREFILTER"]
 
@@ -104,3 +104,63 @@ def coreness_host(rowptr: np.ndarray, colidx: np.ndarray, algo="histocore", flag
                                 ctypes.byref(stats) if stats is not None else None)
     check(rc)
     return out
+
+
+class DynamicCoreness:
+    """Decremental HistoCore (include/pico_dyn.h): the coreness of a graph
+    kept up to date under batches of edge deletions, reusing the persistent
+    per-vertex histograms instead of recomputing from scratch.
+
+        d = pico.DynamicCoreness(rowptr, colidx)      # device CSR
+        d.delete_edges(src, dst)                      # int32 CUDA tensors
+        core = d.coreness()
+    """
+
+    def __init__(self, rowptr, colidx, flags: int = 0, stats: Stats | None = None, stream=None):
+        import torch
+        self.lib = load()
+        if not (rowptr.is_cuda and colidx.is_cuda):
+            raise ValueError("rowptr and colidx must be CUDA tensors (no CPU fallback)")
+        self.dev = rowptr.device
+        self.n = rowptr.numel() - 1
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.dev):
+            check(self.lib.pico_dyn_create(rowptr.contiguous().data_ptr(),
+                                           colidx.contiguous().data_ptr() if colidx.numel() else None,
+                                           self.n, colidx.numel() // 2, flags,
+                                           ctypes.c_void_p(self.stream.cuda_stream),
+                                           ctypes.byref(stats) if stats is not None else None, ctypes.byref(h)))
+        self.h = h
+
+    def coreness(self, out=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.int32, device=self.dev)
+        check(self.lib.pico_dyn_coreness(self.h, out.data_ptr()))
+        return out
+
+    def delete_edges(self, src, dst, stats: Stats | None = None, frontier_sizes=None):
+        import torch
+        src = src.to(device=self.dev, dtype=torch.int32).contiguous()
+        dst = dst.to(device=self.dev, dtype=torch.int32).contiguous()
+        st = stats
+        if frontier_sizes is not None:
+            st = st or Stats()
+            st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            st.frontier_sizes_cap = frontier_sizes.size
+        check(self.lib.pico_dyn_delete_edges(self.h, src.data_ptr() if src.numel() else None,
+                                             dst.data_ptr() if dst.numel() else None, src.numel(),
+                                             ctypes.byref(st) if st is not None else None))
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(self.lib.pico_dyn_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

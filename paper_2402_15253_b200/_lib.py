@@ -119,6 +119,14 @@ def load(path: str | None = None):
     lib.pico_relabel_threshold.argtypes = []
     lib.pico_relabel_threshold.restype = i64
     _setup_shard(lib)
+    lib.pico_dyn_create.argtypes = [vp, vp, i64, i64, u32, vp, ctypes.POINTER(Stats), ctypes.POINTER(vp)]
+    lib.pico_dyn_create.restype = i32
+    lib.pico_dyn_coreness.argtypes = [vp, vp]
+    lib.pico_dyn_coreness.restype = i32
+    lib.pico_dyn_delete_edges.argtypes = [vp, vp, vp, i64, ctypes.POINTER(Stats)]
+    lib.pico_dyn_delete_edges.restype = i32
+    lib.pico_dyn_destroy.argtypes = [vp]
+    lib.pico_dyn_destroy.restype = i32
     _lib = lib
     return lib
 

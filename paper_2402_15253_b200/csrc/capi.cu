@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "pico_shard.h"
+#include "pico_dyn.h"
 
 namespace pico {
 
@@ -717,6 +718,63 @@ int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const i
                           int32_t *core_out_local, pico_stream_t stream) {
     return pico_coreness_sharded_ex(comm, rowptr_local, colidx_local, n_global, m_global, v_begin, v_end, algo,
                                     core_out_local, stream, 0, nullptr);
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// decremental HistoCore (include/pico_dyn.h)
+// ===========================================================================
+struct pico_dyn_s {
+    Dyn *impl;
+};
+
+extern "C" {
+
+int pico_dyn_create(const int64_t *rowptr, const int32_t *colidx, int64_t n, int64_t m, uint32_t flags,
+                    pico_stream_t stream, pico_stats_t *stats, pico_dyn_t *out) {
+    g_last_error.clear();
+    reset_stats(stats);
+    if (!out) return fail(PICO_EINVAL, "NULL output handle");
+    *out = nullptr;
+    if (n <= 0 || m < 0) return fail(PICO_EINVAL, "bad n (%lld) or m (%lld)", (long long)n, (long long)m);
+    if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n = %lld needs 64-bit vertex ids", (long long)n);
+    if (!rowptr || (m > 0 && !colidx)) return fail(PICO_EINVAL, "NULL pointer argument");
+    DevInfo dev;
+    cudaError_t e = dev_info(&dev);
+    if (e) return cuda_fail(e, "device query");
+    if (!dev.coop) return fail(PICO_ENOTSUP, "cooperative launch unavailable");
+    Dyn *impl = nullptr;
+    e = dyn_create((const long long *)rowptr, colidx, n, 2 * (long long)m, flags, (cudaStream_t)stream, dev, stats,
+                   &impl);
+    if (e) return cuda_fail(e, "dyn create");
+    *out = new pico_dyn_s{impl};
+    return PICO_OK;
+}
+
+int pico_dyn_coreness(pico_dyn_t h, int32_t *core_out) {
+    g_last_error.clear();
+    if (!h || !core_out) return fail(PICO_EINVAL, "NULL argument");
+    cudaError_t e = dyn_core(h->impl, core_out);
+    return e ? cuda_fail(e, "dyn coreness") : PICO_OK;
+}
+
+int pico_dyn_delete_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, int64_t k, pico_stats_t *stats) {
+    g_last_error.clear();
+    reset_stats(stats);
+    if (!h || k < 0 || (k > 0 && (!src || !dst))) return fail(PICO_EINVAL, "bad argument");
+    cudaError_t e = dyn_delete(h->impl, src, dst, k, stats);
+    if (e == cudaErrorInvalidValue)
+        return fail(PICO_EINVAL, "a deleted edge is not an edge of the current graph (or a self loop / bad id)");
+    return e ? cuda_fail(e, "dyn delete") : PICO_OK;
+}
+
+int pico_dyn_destroy(pico_dyn_t h) {
+    g_last_error.clear();
+    if (!h) return PICO_OK;
+    cudaError_t e = dyn_destroy(h->impl);
+    delete h;
+    return e ? cuda_fail(e, "dyn destroy") : PICO_OK;
 }
 
 }  // extern "C"

@@ -130,6 +130,9 @@ struct HcArgs {
     // bucket gathers the records of an L2-sized slice of the vertices
     int npass, pshift;
     unsigned long long *boff;  // [kMaxPass + 1] bucket offsets
+    // decremental updates (pico_dyn_*): a vertex that lost every neighbour
+    // walks down to h = 0 instead of flagging a broken invariant
+    int allow_zero;
     int *psrc, *pdst;
 };
 
@@ -1040,6 +1043,7 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
         // (a broken invariant can walk k below 1 here: the warp loop below
         // then stops at once)
         for (int stp = 0; stp < 32; stp++) {
+            if (k == 0 && a.allow_zero) { done = true; break; }  // no neighbour left: h = 0
             sum += __ldcg(a.histo + hb + k);
             if (STATS) st_bins++;
             if (sum >= k) { done = true; break; }
@@ -1068,12 +1072,13 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
                 break;
             }
             if (kL <= 32) {
-                // no bin down to 1 reaches its index: a histogram invariant
-                // is broken (the input is not a symmetric deduplicated
-                // loop-free CSR); stop instead of walking on forever
-                if (lane == 0) *reinterpret_cast<volatile int *>(&a.ctl->error) = 1;
-                rk = 1;
-                rs = 1;
+                // no bin down to 1 reaches its index: the vertex has no
+                // neighbour left (decremental updates: h = 0) or a histogram
+                // invariant is broken (the input is not a symmetric
+                // deduplicated loop-free CSR); stop instead of walking on
+                if (!a.allow_zero && lane == 0) *reinterpret_cast<volatile int *>(&a.ctl->error) = 1;
+                rk = a.allow_zero ? 0 : 1;
+                rs = a.allow_zero ? 0 : 1;
                 break;
             }
             sL += __shfl_sync(FULL, incl, 31);
@@ -1086,7 +1091,7 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
         a.core[v] = k;
         a.rec[v] = pack_rec(k, cold);
         a.oldc[v] = cold;
-        a.histo[hb + k] = sum;  // cap bin := cnt
+        if (k > 0) a.histo[hb + k] = sum;  // cap bin := cnt
         int L = scan_len(a, hb + 1, (int)d, k);
         a.slen[v] = L;
         nseg = nseg_of(L, a.tn.seg);
@@ -1385,8 +1390,9 @@ struct Timer {
 template <bool STATS>
 static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, long long arcs,
                             int *core, cudaStream_t s, uint32_t flags, void *ws,
-                            pico_stats_t *st, const DevInfo &dev) {
+                            pico_stats_t *st, const DevInfo &dev, HcArgs *keep = nullptr) {
     HcArgs a;
+    a.allow_zero = 0;
     Tune tn = hc_tune(flags);
     HcLayout L = hc_layout(n, arcs, flags);
     char *p = (char *)ws;
@@ -1617,6 +1623,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         }
     }
     tm.collect(st);
+    if (keep) *keep = a;
     return cudaSuccess;
 }
 
@@ -2089,6 +2096,201 @@ cudaError_t shard_result(Shard *h, int *core_out) {
 }
 
 cudaError_t shard_destroy(Shard *h) {
+    cudaError_t e = cudaFreeAsync(h->ws, h->s);
+    if (!e) e = cudaStreamSynchronize(h->s);
+    delete h;
+    return e;
+}
+
+// ===========================================================================
+// Decremental HistoCore (the
+// Index2core paradigm suits dynamic graphs).  After a run, the state kept in
+// the workspace -- estimates equal to the coreness, every histogram exact
+// (bins below the coreness count neighbours of that coreness, the cap bin
+// the neighbours at or above it) -- is reused for batches of edge deletions:
+//   1. each deleted arc (x, y) becomes a tombstone: a self-loop (x, x) in the
+//      owned CSR copy and in the pull edge list; a self-loop never passes the
+//      UpdateHisto guard core[u] > core[v], so no kernel needs a new test;
+//   2. y's contribution leaves x's histogram (the cap bin if core[y] >=
+//      core[x], marking x as a frontier candidate, else bin core[y]);
+//   3. the usual rounds run from the marked vertices.
+// A deletion can only lower coreness, so the old coreness is an upper bound
+// of the new one and the Index2core iteration from it converges to the new
+// coreness (the largest fixed point below the start; readings in DESIGN.md).
+// ===========================================================================
+__global__ void dyn_delete_kernel(HcArgs a, int *ci_own, const int *src, const int *dst, long long k, int *err) {
+    const int lane = lane_id();
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = gw; i < k; i += nw) {
+        const int eu = src[i], ev = dst[i];
+        for (int dir = 0; dir < 2; dir++) {
+            const int x = dir ? ev : eu, y = dir ? eu : ev;
+            if (x < 0 || x >= a.n || y < 0 || y >= a.n || x == y) {
+                if (lane == 0) atomicOr(err, 1);
+                continue;
+            }
+            // the arc (x, y) in the owned CSR row of x
+            const long long r0 = a.rp[x], r1 = a.rp[x + 1];
+            long long pos = -1;
+            for (long long e0 = r0; e0 < r1; e0 += 32) {
+                long long e = e0 + lane;
+                unsigned m = __ballot_sync(FULL, e < r1 && ci_own[e] == y);
+                if (m) {
+                    pos = e0 + __ffs(m) - 1;
+                    break;
+                }
+            }
+            if (pos < 0) {
+                if (lane == 0) atomicOr(err, 2);  // not an edge of the current graph
+                continue;
+            }
+            if (lane == 0) ci_own[pos] = x;  // tombstone (one bucket: pdst is ci_own)
+            if (a.npass > 1) {
+                // the arc in bucket y >> pshift of the edge list (CSR order: a
+                // binary search for x's run, then a warp scan of the run)
+                const int p = y >> a.pshift;
+                long long lo = (long long)a.boff[p], hi = (long long)a.boff[p + 1];
+                while (lo < hi) {
+                    long long mid = (lo + hi) >> 1;
+                    if (a.psrc[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                const long long be = (long long)a.boff[p + 1];
+                for (long long e0 = lo; e0 < be; e0 += 32) {
+                    long long e = e0 + lane;
+                    bool in = e < be && a.psrc[e] == x;
+                    unsigned m = __ballot_sync(FULL, in && a.pdst[e] == y);
+                    if (m) {
+                        if (lane == __ffs(m) - 1) a.pdst[e] = x;
+                        break;
+                    }
+                    if (__ballot_sync(FULL, in) != FULL) break;  // past x's run
+                }
+            }
+            // y leaves x's histogram
+            if (lane == 0) {
+                const int cx = a.core[x], cy = a.core[y];
+                const long long hb = r0 - 1;
+                if (cy >= cx) {
+                    atomicSub(a.histo + hb + cx, 1);  // cnt(x) drops: a frontier candidate
+                    atomicOr(a.capd + (x >> 5), 1u << (x & 31));
+                } else {
+                    atomicSub(a.histo + hb + cy, 1);
+                }
+            }
+        }
+    }
+}
+
+struct Dyn {
+    HcArgs a;
+    void *ws;
+    long long *rp;
+    int *ci;
+    int *core;
+    long long n, arcs;
+    uint32_t flags;
+    cudaStream_t s;
+    DevInfo dev;
+    int *err;
+};
+
+size_t dyn_workspace_bytes(long long n, long long arcs, uint32_t flags) {
+    return align256(hc_workspace_bytes(n, arcs, flags)) + align256(sizeof(long long) * (size_t)(n + 1)) +
+           align256(sizeof(int) * (size_t)std::max(arcs, 1ll)) + align256(sizeof(int) * (size_t)std::max(n, 1ll)) +
+           256;
+}
+
+cudaError_t dyn_create(const long long *rp, const int *ci, long long n, long long arcs, uint32_t flags,
+                       cudaStream_t s, const DevInfo &dev, pico_stats_t *st, Dyn **out) {
+    Dyn *h = new Dyn();
+    h->n = n; h->arcs = arcs; h->flags = flags & ~(uint32_t)(PICO_F_STATS | PICO_F_HOST_LOOP); h->s = s; h->dev = dev;
+    cudaError_t e = cudaMallocAsync(&h->ws, dyn_workspace_bytes(n, arcs, h->flags), s);
+    if (e) { delete h; return e; }
+    char *p = (char *)h->ws + align256(hc_workspace_bytes(n, arcs, h->flags));
+    h->rp = (long long *)p; p += align256(sizeof(long long) * (size_t)(n + 1));
+    h->ci = (int *)p; p += align256(sizeof(int) * (size_t)std::max(arcs, 1ll));
+    h->core = (int *)p; p += align256(sizeof(int) * (size_t)std::max(n, 1ll));
+    h->err = (int *)p;
+    if (!e) e = cudaMemcpyAsync(h->rp, rp, sizeof(long long) * (size_t)(n + 1), cudaMemcpyDeviceToDevice, s);
+    if (!e && arcs) e = cudaMemcpyAsync(h->ci, ci, sizeof(int) * (size_t)arcs, cudaMemcpyDeviceToDevice, s);
+    if (!e) e = hc_run_t<false>(h->rp, h->ci, n, arcs, h->core, s, h->flags, h->ws, st, dev, &h->a);
+    if (e) {
+        cudaFreeAsync(h->ws, s);
+        cudaStreamSynchronize(s);
+        delete h;
+        return e;
+    }
+    *out = h;
+    return cudaSuccess;
+}
+
+cudaError_t dyn_core(Dyn *h, int *core_out) {
+    cudaError_t e = cudaMemcpyAsync(core_out, h->core, sizeof(int) * (size_t)h->n, cudaMemcpyDeviceToDevice, h->s);
+    if (!e) e = cudaStreamSynchronize(h->s);
+    return e;
+}
+
+// returns cudaErrorInvalidValue for an edge that is not in the current graph
+cudaError_t dyn_delete(Dyn *h, const int *src, const int *dst, long long k, pico_stats_t *st) {
+    cudaStream_t s = h->s;
+    HcArgs &a = h->a;
+    const int sms = h->dev.sms;
+    cudaError_t e;
+    Ctrl hc{};
+    hc.mincv[0] = hc.mincv[1] = INT_MAX;
+    if ((e = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return e;
+    if ((e = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)a.nwords, s))) return e;
+    if ((e = cudaMemsetAsync(a.capd, 0, sizeof(unsigned) * (size_t)a.nwords, s))) return e;
+    if ((e = cudaMemsetAsync(h->err, 0, sizeof(int), s))) return e;
+    if (k > 0) dyn_delete_kernel<<<sms * 8, 256, 0, s>>>(a, h->ci, src, dst, k, h->err);
+    int herr = 0;
+    if ((e = cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (herr) return cudaErrorInvalidValue;
+    a.allow_zero = 1;
+    // SumHisto of the marked vertices -> C_1, then the rounds
+    hc_collect_sum_kernel<false><<<sms * 4, 512, 0, s>>>(a, 1);
+    unsigned long long c1 = 0;
+    if ((e = cudaMemcpyAsync(&c1, &a.ctl->nF[1], sizeof(c1), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    std::vector<long long> sizes;
+    if (c1) sizes.push_back((long long)c1);
+    if ((e = cudaMemsetAsync(&a.ctl->nF[1], 0, sizeof(unsigned long long), s))) return e;
+    long long launches = 2;
+    if (c1) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hc_rounds_kernel<false>, 512, 0);
+        void *args[] = {&a};
+        if ((e = cudaLaunchCooperativeKernel((const void *)hc_rounds_kernel<false>, sms * std::max(1, occ), 512,
+                                             args, 0, s)))
+            return e;
+        launches++;
+        unsigned long long devrounds = 0;
+        int derr = 0;
+        if ((e = cudaMemcpyAsync(&devrounds, &a.ctl->rounds, sizeof(devrounds), cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaMemcpyAsync(&derr, &a.ctl->error, sizeof(derr), cudaMemcpyDeviceToHost, s))) return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        if (derr) return cudaErrorAssert;
+        size_t nr = (size_t)std::min<unsigned long long>(devrounds + 2, kFszCap);
+        std::vector<unsigned long long> dsz(nr, 0);
+        if ((e = cudaMemcpyAsync(dsz.data(), a.fsz, sizeof(unsigned long long) * nr, cudaMemcpyDeviceToHost, s)))
+            return e;
+        if ((e = cudaStreamSynchronize(s))) return e;
+        for (unsigned long long t = 1; t <= devrounds && t < kFszCap; t++) sizes.push_back((long long)dsz[t]);
+    }
+    if ((e = cudaGetLastError())) return e;
+    if (st) {
+        st->rounds = (int64_t)sizes.size();
+        st->kernel_count += launches;
+        if (st->frontier_sizes)
+            for (size_t i = 0; i < sizes.size() && (int64_t)i < st->frontier_sizes_cap; i++)
+                st->frontier_sizes[i] = sizes[i];
+    }
+    return cudaSuccess;
+}
+
+cudaError_t dyn_destroy(Dyn *h) {
     cudaError_t e = cudaFreeAsync(h->ws, h->s);
     if (!e) e = cudaStreamSynchronize(h->s);
     delete h;

@@ -59,6 +59,14 @@ cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long
 cudaError_t shard_result(Shard *h, int *core_out);
 cudaError_t shard_destroy(Shard *h);
 
+// decremental HistoCore (histocore.cu)
+struct Dyn;
+cudaError_t dyn_create(const long long *rp, const int *ci, long long n, long long arcs, uint32_t flags,
+                       cudaStream_t s, const DevInfo &dev, pico_stats_t *st, Dyn **out);
+cudaError_t dyn_core(Dyn *h, int *core_out);
+cudaError_t dyn_delete(Dyn *h, const int *src, const int *dst, long long k, pico_stats_t *st);
+cudaError_t dyn_destroy(Dyn *h);
+
 size_t validate_workspace_bytes();
 cudaError_t validate_run(const long long *rp, const int *ci, long long n, long long arcs,
                          cudaStream_t s, void *ws, int *bad);

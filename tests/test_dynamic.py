@@ -1,0 +1,64 @@
+"""Decremental HistoCore (include/pico_dyn.h): after
+every batch of edge deletions the maintained coreness equals the BZ oracle's
+coreness of the reduced graph, element by element, for the default schedule
+and for forced pull rounds over a multi-bucket edge list (tombstones in both
+the CSR copy and the edge list) and forced push rounds; a vertex that loses
+every edge drops to coreness 0; a missing edge is rejected."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _edges(rp, ci):
+    src = np.repeat(np.arange(rp.size - 1), np.diff(rp))
+    keep = src < ci
+    return np.stack([src[keep], ci[keep]], 1)
+
+
+def _reduced(n, edges):
+    rp, ci = synth.from_edge_list(n, [tuple(e) for e in edges.tolist()])
+    return synth.to_numpy(rp, ci)
+
+
+@pytest.mark.parametrize("cfg,flags", [("R12", 0), ("R12", 128 | 32), ("R12", 64), ("R14", 0)])
+def test_decremental_batches(cfg, flags):
+    import torch
+    import paper_2402_15253_b200 as pico
+    dev = torch.device("cuda:0")
+    rp, ci = synth.to_numpy(*synth.CONFIGS[cfg].build())
+    n = rp.size - 1
+    edges = _edges(rp, ci)
+    rng = np.random.default_rng(11)
+    d = pico.DynamicCoreness(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), flags=flags)
+    try:
+        assert np.array_equal(d.coreness().cpu().numpy(), oracle.bz(rp, ci))
+        # a hub loses every edge; then random batches of growing size
+        hub = int(np.argmax(np.diff(rp)))
+        batches = [np.flatnonzero((edges[:, 0] == hub) | (edges[:, 1] == hub))]
+        alive = np.ones(len(edges), bool)
+        alive[batches[0]] = False
+        for size in (1, 17, len(edges) // 20, len(edges) // 5):
+            idx = rng.choice(np.flatnonzero(alive), size=min(size, int(alive.sum())), replace=False)
+            alive[idx] = False
+            batches.append(idx)
+        alive = np.ones(len(edges), bool)
+        for b in batches:
+            e = edges[b]
+            d.delete_edges(torch.from_numpy(e[:, 0].astype(np.int32)), torch.from_numpy(e[:, 1].astype(np.int32)))
+            alive[b] = False
+            r_rp, r_ci = _reduced(n, edges[alive])
+            ref = oracle.bz(r_rp, r_ci)
+            got = d.coreness().cpu().numpy()
+            assert np.array_equal(got, ref), (cfg, flags, int((got != ref).sum()))
+        assert d.coreness()[hub].item() == 0
+        # an edge that is no longer in the graph
+        e = edges[batches[-1][:1]]
+        with pytest.raises(pico.PicoError) as ei:
+            d.delete_edges(torch.from_numpy(e[:, 0].astype(np.int32)), torch.from_numpy(e[:, 1].astype(np.int32)))
+        assert ei.value.status == 1
+    finally:
+        d.close()
