@@ -1244,14 +1244,6 @@ __global__ void __launch_bounds__(512, 2) hc_collect_sum_kernel(HcArgs a, int t)
     collect_sum_phase<STATS>(a, t);
 }
 
-// sharded rounds: SumHisto over the pushed frontier list
-template <bool STATS>
-__global__ void __launch_bounds__(512) hc_sum_kernel(HcArgs a, int t) {
-    const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nthreads = (long long)gridDim.x * blockDim.x;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->nF[(t + 1) & 1] = 0;
-    sum_phase<STATS>(a, t, gthread, nthreads);
-}
 
 // ---------------------------------------------------------------------------
 // host driver
