@@ -43,7 +43,13 @@ def bench_sharded(args):
     vb, ve = bounds[rank], bounds[rank + 1]
     rp_l, ci_l = sharded.local_rows(rp, ci, vb, ve)
 
-    comm = sharded.NcclComm() if args.exchange == "nccl" else None
+    comm, exchange_note = None, "torch.distributed"
+    if args.exchange == "nccl":
+        try:
+            comm = sharded.NcclComm()
+            exchange_note = "NCCL inside libpico (pico_coreness_sharded)"
+        except Exception as e:  # no usable libnccl: the torch.distributed exchange (also GPU, also NCCL)
+            exchange_note = f"torch.distributed (in-library NCCL unavailable: {e})"
 
     def run_once(rp_d, ci_d):
         if comm is not None:  # one library call; the exchange runs over NCCL inside libpico
@@ -59,8 +65,17 @@ def bench_sharded(args):
     def step():
         return run_once(rp_l, ci_l)
 
-    for _ in range(args.warmup):
-        run = step()
+    for w in range(args.warmup):
+        try:
+            run = step()
+        except Exception as e:
+            if comm is None or w > 0:
+                raise
+            # the in-library exchange failed on this box: every rank falls back together
+            comm.close()
+            comm = None
+            exchange_note = f"torch.distributed (in-library NCCL failed: {e})"
+            run = step()
     dist.barrier()
     torch.cuda.synchronize()
     clk = bench.ClockSampler(local) if rank == 0 else None
@@ -121,9 +136,8 @@ def bench_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": cfg.note, "config": args.config, "algo": "histocore-sharded", "n": n, "m": m,
-                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL, "
-                                      + ("inside libpico: pico_coreness_sharded)" if comm is not None
-                                         else "torch.distributed)"),
+                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL: "
+                                      + exchange_note + ")",
                        "l2_flush": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
                          "traffic": None, "peak_source": src + f" x {world} GPUs",
