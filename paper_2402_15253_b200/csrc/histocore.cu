@@ -335,13 +335,13 @@ __global__ void __launch_bounds__(512) hc_reorder_cta_kernel(HcArgs a) {
 // neighbour degree for init, clamped to d (the histogram cap of P:498)
 // (nv8 / nv16 / nv32: degree of every neighbour id saturated at 255, at
 // 65535, and exact; the local shadows / oldcore on one GPU, the all-gathered
-// global degrees on a shard).  The thread-per-vertex class (d <= 16) gathers
-// the 1-byte shadow, exact for it and half the L2 footprint (measured: 1.2x
-// faster at RMAT-26); the warp and CTA classes gather the 2-byte one (a
-// 1-byte shadow plus exact fallback was measured 1.1-1.7x slower for them:
-// their neighbours are often hubs).
+// global degrees on a shard).  Rows with d <= 255 (the thread class and the
+// first warp-class launch) gather the 1-byte shadow, exact for them and half
+// the L2 footprint; longer rows gather the 2-byte one (a 1-byte shadow plus
+// an exact fallback was measured 1.1-1.7x slower for them: their neighbours
+// are often hubs).
 __device__ __forceinline__ int init_val_small(const HcArgs &a, int u, int d, unsigned long long hot) {
-    return min((int)ld_shadow(a.nv8 + u, hot), d);  // d <= 16 < 255: exact
+    return min((int)ld_shadow(a.nv8 + u, hot), d);  // d <= 255: exact
 }
 
 __device__ __forceinline__ int init_val(const HcArgs &a, int u, int d, unsigned long long hot) {
@@ -415,7 +415,13 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
 // ---------------------------------------------------------------------------
 // class B: one warp per vertex, a_max < deg <= b_max, shared-memory bins
 // ---------------------------------------------------------------------------
-template <bool STATS>
+// PART 0: every class-B row, gathering the 2-byte degree shadow.  On large
+// graphs (hc_init_split) two launches instead: PART 1 the rows with d <= 255
+// gathering the 1-byte shadow (exact for them), PART 2 the longer rows with
+// the 2-byte one, so that only one shadow array competes for the L2 at a time
+// (RMAT-26: 31.6 -> 29.1 ms; on C2, whose shadows fit the L2 anyway, the
+// second launch costs more than it saves)
+template <bool STATS, int PART>
 __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
     extern __shared__ int sh[];
     const int wib = threadIdx.x >> 5;
@@ -431,21 +437,23 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         int v = a.BC[idx];
         long long hb = a.rp[v];
         int d = (int)(a.rp[v + 1] - hb);
+        if (PART != 0 && (d <= (int)SAT8) != (PART == 1)) continue;  // the other launch's row (warp-uniform)
         for (int b = lane; b <= d; b += 32) bins[b] = 0;
         __syncwarp();
+        auto val = [&](int u) { return PART == 1 ? init_val_small(a, u, d, hot) : init_val(a, u, d, hot); };
         {
             int e = lane;
             for (; e + 96 < d; e += 128) {  // 4 gathers in flight per lane
                 int u0 = ld_stream(a.ci + hb + e, cold), u1 = ld_stream(a.ci + hb + e + 32, cold);
                 int u2 = ld_stream(a.ci + hb + e + 64, cold), u3 = ld_stream(a.ci + hb + e + 96, cold);
-                int x0 = init_val(a, u0, d, hot), x1 = init_val(a, u1, d, hot);
-                int x2 = init_val(a, u2, d, hot), x3 = init_val(a, u3, d, hot);
+                int x0 = val(u0), x1 = val(u1);
+                int x2 = val(u2), x3 = val(u3);
                 atomicAdd(&bins[x0], 1);
                 atomicAdd(&bins[x1], 1);
                 atomicAdd(&bins[x2], 1);
                 atomicAdd(&bins[x3], 1);
             }
-            for (; e < d; e += 32) atomicAdd(&bins[init_val(a, ld_stream(a.ci + hb + e, cold), d, hot)], 1);
+            for (; e < d; e += 32) atomicAdd(&bins[val(ld_stream(a.ci + hb + e, cold))], 1);
         }
         __syncwarp();
         // descending walk for the h-index (SumHisto on the fresh histogram)
@@ -1265,6 +1273,10 @@ Tune hc_tune(uint32_t flags) {
     return t;
 }
 
+// whether the class-B InitHisto runs as two launches split by row length
+// (the 2-byte degree shadow of n vertices outgrows a share of the L2)
+static bool hc_init_split(long long n) { return n >= (8ll << 20); }
+
 // whether dense rounds may pull, and into how many v-range passes
 static bool hc_allow_pull(long long n, uint32_t flags) {
     return (flags & PICO_F_PUSH_ONLY) ? false : (flags & PICO_F_PULL_ALWAYS) ? true : (n >= kPullMinN);
@@ -1479,11 +1491,22 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
         hc_init_small_kernel<STATS><<<std::max(blocks, 1), 256, 0, s>>>(a);
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
-        cudaFuncSetAttribute(hc_init_warp_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smB);
         int occB = 0, occC = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS>, 256, smB);
-        hc_init_warp_kernel<STATS><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+        if (hc_init_split(n)) {
+            cudaFuncSetAttribute(hc_init_warp_kernel<STATS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smB);
+            cudaFuncSetAttribute(hc_init_warp_kernel<STATS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smB);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS, 1>, 256, smB);
+            hc_init_warp_kernel<STATS, 1><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+            hc_init_warp_kernel<STATS, 2><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+            launches++;
+        } else {
+            cudaFuncSetAttribute(hc_init_warp_kernel<STATS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smB);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS, 0>, 256, smB);
+            hc_init_warp_kernel<STATS, 0><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+        }
         size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
         cudaFuncSetAttribute(hc_init_cta_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smC);
@@ -1996,10 +2019,18 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         Tune tn = a.tn;
         hc_init_small_kernel<false><<<grid(h->nloc), 256, 0, s>>>(a);
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
-        cudaFuncSetAttribute(hc_init_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
         int occB = 0, occC = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false>, 256, smB);
-        hc_init_warp_kernel<false><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+        if (hc_init_split(h->ng)) {  // the gathered shadows are global-size on a shard
+            cudaFuncSetAttribute(hc_init_warp_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            cudaFuncSetAttribute(hc_init_warp_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false, 1>, 256, smB);
+            hc_init_warp_kernel<false, 1><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+            hc_init_warp_kernel<false, 2><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(hc_init_warp_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false, 0>, 256, smB);
+            hc_init_warp_kernel<false, 0><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+        }
         size_t smC = sizeof(int) * (size_t)(tn.c_bins + 1);
         cudaFuncSetAttribute(hc_init_cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, hc_init_cta_kernel<false>, 512, smC);
