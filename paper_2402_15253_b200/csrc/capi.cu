@@ -675,10 +675,11 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
         // rounds
         long long rounds = 0;
         for (;;) {
-            long long c = 0;
-            if ((e = shard_pack(sh, trip, std::max(nloc, 1ll), &c))) { bail_cuda(e, "shard pack"); break; }
-            if ((e = cudaMemcpyAsync(cnt, &c, sizeof(long long), cudaMemcpyHostToDevice, s))) { bail_cuda(e, "count"); break; }
-            if ((nr = N.AllGather(cnt, cnt + 1, 1, ncclInt64, comm->c, s)) != ncclSuccess) { bail_nccl(nr, "allgather counts"); break; }
+            // pack, then all-gather the counts straight from device memory: one host
+            // synchronisation per round (the grouped broadcasts need host counts)
+            const unsigned long long *cdev = nullptr;
+            if ((e = shard_pack_dev(sh, trip, &cdev))) { bail_cuda(e, "shard pack"); break; }
+            if ((nr = N.AllGather(cdev, cnt + 1, 1, ncclInt64, comm->c, s)) != ncclSuccess) { bail_nccl(nr, "allgather counts"); break; }
             if ((e = cudaMemcpyAsync(hc.data(), cnt + 1, sizeof(long long) * P, cudaMemcpyDeviceToHost, s)) ||
                 (e = cudaStreamSynchronize(s))) { bail_cuda(e, "counts"); break; }
             for (int r = 0; r < P; r++) off[r + 1] = off[r] + hc[r];

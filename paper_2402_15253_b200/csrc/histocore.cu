@@ -2063,6 +2063,17 @@ cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count) 
     return cudaGetLastError();
 }
 
+// stream-ordered pack: the count stays on the device (*count_dev; read by a
+// collective, not by the host)
+cudaError_t shard_pack_dev(Shard *h, int *triples, const unsigned long long **count_dev) {
+    cudaStream_t s = h->s;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(h->cnt, 0, sizeof(unsigned long long), s))) return e;
+    sh_pack_kernel<<<h->dev.sms * 4, 256, 0, s>>>(h->a, &h->a.ctl->nS[h->t & 1], h->vb, triples, h->cnt);
+    *count_dev = h->cnt;
+    return cudaGetLastError();
+}
+
 // UpdateHisto(C_t of all ranks) -- push over the local CSC, or, for dense
 // rounds, pull over the bucketed local edge list against the global records
 // -- then SumHisto of the local frontier.  The direction is decided on the
