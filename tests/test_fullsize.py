@@ -55,3 +55,24 @@ def test_full_size_social(cfg):
 @pytest.mark.parametrize("cfg", ["T", "C4"])
 def test_full_size_billion_edges(cfg):
     _check(cfg, kcore=False)
+
+
+@pytest.mark.parametrize("parts", [2, 4])
+def test_full_size_sharded_loopback(parts):
+    """The sharded path (pull rounds over the rank edge lists and push rounds
+    over the rank CSCs, gated per round) on the full C2 graph, P logical
+    shards on one GPU, against the BZ oracle; l2 and every global |C_t| equal
+    the single-GPU run's."""
+    import torch
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import sharded
+    rp, ci = _graph("C2")
+    ref = oracle.bz(*synth.to_numpy(rp, ci))
+    core, rounds, sizes = sharded.coreness_loopback(rp, ci, parts)
+    assert np.array_equal(core.cpu().numpy(), ref)
+    st = pico.Stats()
+    fs = np.zeros(1 << 12, dtype=np.int64)
+    pico.coreness(rp, ci, stats=st, frontier_sizes=fs)
+    assert rounds == st.rounds and sizes == [int(x) for x in fs[:st.rounds]]
+    del rp, ci
+    torch.cuda.empty_cache()
