@@ -896,9 +896,18 @@ __device__ void update_phase(const HcArgs &a, int t) {
         for (int j0 = 0; j0 < total; j0 += 32 * UA) {
             ArcStep<UA> cur = nx;
             if (PICO_ARC_PF && j0 + 32 * UA < total) arc_fetch<UA>(nx, j0 + 32 * UA, total, excl, b, rows, cold);
+            // the UA record gathers are issued back to back (a fallback load
+            // between them would serialise them: ncu showed each gather waited
+            // for before the next one issued); saturated halves resolve after
             int cu[UA];
+            unsigned rr[UA];
 #pragma unroll
-            for (int q = 0; q < UA; q++) cu[q] = cur.v[q] >= 0 ? core_of(a, cur.v[q], hot) : 0;
+            for (int q = 0; q < UA; q++) rr[q] = cur.v[q] >= 0 ? ld_rec(a.rec + cur.v[q], hot) : 0u;
+#pragma unroll
+            for (int q = 0; q < UA; q++) {
+                cu[q] = (int)(rr[q] & 0xffffu);
+                if (cu[q] == (int)RSAT) cu[q] = __ldcg(a.core + cur.v[q]);
+            }
             int cvo[UA], ovo[UA];
             long long hb[UA];
             // all histogram bases are loaded before the first RED (the REDs'
