@@ -79,7 +79,7 @@ constexpr int kMaxPass = 8;
 // class-C InitHisto shared-memory bins (a vertex whose h-index reaches the
 // cap is redone with global bins; h_1 <= the graph's degree h-index)
 #ifndef PICO_CBINS
-#define PICO_CBINS 16384
+#define PICO_CBINS 8192
 #endif
 #ifndef PICO_ROUNDS_MINB
 #define PICO_ROUNDS_MINB 2         // resident 512-thread CTAs per SM of the round kernel
