@@ -78,6 +78,9 @@ constexpr unsigned RSAT = 65535;   // estimate-record half saturation
 constexpr int kMaxPass = 8;
 // class-C InitHisto shared-memory bins (a vertex whose h-index reaches the
 // cap is redone with global bins; h_1 <= the graph's degree h-index)
+#ifndef PICO_BMAX
+#define PICO_BMAX 2048             // warp-class InitHisto rows: a_max < deg <= PICO_BMAX
+#endif
 #ifndef PICO_CBINS
 #define PICO_CBINS 8192
 #endif
@@ -1272,7 +1275,7 @@ Tune hc_tune(uint32_t flags) {
     if (flags & PICO_F_TINY_TILES) {
         t.a_max = 4; t.b_max = 12; t.c_bins = 16; t.seg = 4;
     } else {
-        t.a_max = 16; t.b_max = 1024; t.c_bins = PICO_CBINS; t.seg = PICO_HC_SEG;
+        t.a_max = 16; t.b_max = PICO_BMAX; t.c_bins = PICO_CBINS; t.seg = PICO_HC_SEG;
     }
 #ifndef PICO_PULL_DIV
 #define PICO_PULL_DIV 2
