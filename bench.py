@@ -277,6 +277,7 @@ def bench_single(args):
     # finish in seconds
     if args.ablations == "on" or (args.ablations == "auto" and 2 * m <= (320 << 20)):
         algos += ["cntcore", "nbrcore"]
+    algos = list(dict.fromkeys(algos))  # (the main algorithm first, once)
     core_ref = None
     for algo in algos:
         # untimed instrumented run: iteration counts + work counters for B_alg
@@ -313,9 +314,10 @@ def bench_single(args):
         ms = e0.elapsed_time(e1) / args.steps
         kms = {k: v / args.steps for k, v in acc["ms"].items()}
         rl = "relabel" in kms
-        if algo == "histocore":
+        ran = {0: "histocore", 1: "peelone"}.get(sd.get("algo"), algo) if algo == "auto" else algo
+        if ran == "histocore":
             byts = hc_bytes(n, m, sd, int(fs[0]) if sd["rounds"] > 0 else 0, rl)
-        elif algo == "peelone":
+        elif ran == "peelone":
             byts = po_bytes(n, m, sd, rl)
         else:
             byts = i2c_bytes(n, m, sd, rl)
@@ -400,7 +402,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--algo", default="histocore", choices=["histocore", "peelone"])
+    ap.add_argument("--algo", default="histocore", choices=["histocore", "peelone", "auto", "cntcore", "nbrcore"])
     ap.add_argument("--impl", default="pico", choices=["pico", "reference"])
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--no-both", dest="both", action="store_false")
