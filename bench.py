@@ -109,15 +109,19 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config: str, algo: str, slot: str):
-    """Per-launch DRAM bytes of a kernel slot from the committed ncu summary."""
+def ncu_slot(config: str, algo: str, slot: str):
+    """The committed ncu summary of a kernel slot (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d[config][algo][slot]["dram_bytes_per_step"]
+            return json.load(f)[config][algo][slot]
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic(config: str, algo: str, slot: str):
+    """Per-launch DRAM bytes of a kernel slot from the committed ncu summary."""
+    return ncu_slot(config, algo, slot).get("dram_bytes_per_step")
 
 
 # ---------------------------------------------------------------------------
@@ -336,7 +340,10 @@ def bench_single(args):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": ncu_traffic(args.config, algo, dom),
                          "peak_source": peak_src,
-                         "whole_step_frac": total_b / (ms * 1e-3) / 1e9 / peak},
+                         "whole_step_frac": total_b / (ms * 1e-3) / 1e9 / peak,
+                         # the second ceiling: L2 throughput of the same kernel, % of
+                         # peak, time-weighted over its ncu capture (profiles/ncu_traffic.json)
+                         "l2_throughput_pct": ncu_slot(args.config, algo, dom).get("l2_throughput_pct")},
             "gpu_launches": acc["count"] // max(args.steps, 1) * args.steps,
             "clocks": clk.summary(),
         }

@@ -78,9 +78,12 @@ def main():
         lines.append((name[:60], slot, vals))
         if slot is None:
             continue
-        a = agg.setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": []})
+        a = agg.setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": [], "l2w": 0.0})
         a["dram_bytes_per_step"] += vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0)
         a["time_s"] += vals.get("gpu__time_duration.sum", 0)
+        # time-weighted L2 throughput (% of peak) of the slot's kernels: the second ceiling
+        a["l2w"] += vals.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", 0) * vals.get(
+            "gpu__time_duration.sum", 0)
         a["kernels"].append(name[:60])
     try:
         with open(out) as f:
@@ -89,6 +92,7 @@ def main():
         allj = {}
     allj.setdefault(cfg, {})[algo] = {k: {"dram_bytes_per_step": v["dram_bytes_per_step"],
                                           "ncu_time_s": v["time_s"], "kernels": v["kernels"],
+                                          "l2_throughput_pct": v["l2w"] / v["time_s"] if v["time_s"] else None,
                                           "source": rep} for k, v in agg.items()}
     with open(out, "w") as f:
         json.dump(allj, f, indent=1, sort_keys=True)
