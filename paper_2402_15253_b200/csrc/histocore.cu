@@ -1868,7 +1868,7 @@ __global__ void __launch_bounds__(512) sh_sum_kernel(HcArgs a, int t, const unsi
 static size_t sort_bytes(long long arcs) {
     size_t b = 0;
     cub::DeviceRadixSort::SortPairs((void *)nullptr, b, (const int *)nullptr, (int *)nullptr, (const int *)nullptr,
-                                    (int *)nullptr, (int)std::max(arcs, 1ll));
+                                    (int *)nullptr, (long long)std::max(arcs, 1ll));  // 64-bit item count
     return b;
 }
 
@@ -1900,7 +1900,6 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     cudaError_t e = cudaMemcpyAsync(&h->arcs, rp + nloc, sizeof(long long), cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     if (e) { delete h; return e; }
-    if (h->arcs > INT_MAX) { delete h; return cudaErrorNotSupported; }  // 32-bit sort / scan counts
     size_t bytes = shard_workspace_bytes(nloc, ng, h->arcs, flags, &h->tscap, &h->cubbytes);
     if ((e = cudaMallocAsync(&h->ws, bytes, s))) { delete h; return e; }
     HcLayout L = hc_layout(nloc, h->arcs, flags, ng, 8);
@@ -2020,7 +2019,7 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         int bits = 1;
         while ((1ll << bits) < h->ng) bits++;
         cb = h->cubbytes;
-        if ((e = cub::DeviceRadixSort::SortPairs(h->cubtmp, cb, a.ci, h->tmpk, src, h->csc_idx, (int)h->arcs, 0,
+        if ((e = cub::DeviceRadixSort::SortPairs(h->cubtmp, cb, a.ci, h->tmpk, src, h->csc_idx, (long long)h->arcs, 0,
                                                  bits, s)))
             return e;
     } else {
