@@ -1232,7 +1232,9 @@ __global__ void __launch_bounds__(512, PICO_ROUNDS_MINB) hc_rounds_kernel(HcArgs
         if (leader && (unsigned long long)t < a.fsz_cap) a.rtime[2 * t] = globaltimer();
         unsigned long long nf = bcast_u64(&a.ctl->nF[(t + 1) & 1]);
         if (nf == 0) break;
-        if ((unsigned long long)t + 1 >= a.fsz_cap) {  // far beyond any valid l2: broken input
+        // every round lowers the sum of the estimates, so a valid run has l2 <= 2m rounds
+        // (a long path needs ~n/2, far beyond the recorded kFszCap); more is broken input
+        if ((unsigned long long)t > (unsigned long long)a.arcs + 2) {
             if (leader) *reinterpret_cast<volatile int *>(&a.ctl->error) = 1;
             break;
         }
@@ -1569,7 +1571,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                 if (nf == 0) break;
                 rounds++;
                 hsz.push_back(nf);
-                if ((unsigned long long)t + 1 >= kFszCap) return cudaErrorAssert;  // broken input
+                if ((unsigned long long)t > (unsigned long long)arcs + 2) return cudaErrorAssert;  // broken input
             }
             int derr = 0;
             if ((err = cudaMemcpyAsync(&derr, &a.ctl->error, sizeof(derr), cudaMemcpyDeviceToHost, s))) return err;

@@ -385,7 +385,7 @@ cudaError_t i2c_run(const long long *rp, const int *ci, long long n, long long a
         i2c_compact_kernel<<<grid(a.nwords), 256, 0, s>>>(a);
         launches += 3;
         if ((e = cudaGetLastError())) return e;
-        if (sizes.size() >= kFszCap) return cudaErrorAssert;  // far beyond any valid l2: broken input
+        if ((long long)sizes.size() > arcs + 2) return cudaErrorAssert;  // beyond any valid l2 (<= 2m): broken input
     }
     if ((e = cudaGetLastError())) return e;
     if (timing) {

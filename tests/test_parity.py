@@ -255,3 +255,19 @@ def test_index2core_ablations(algo):
 
 def pico_flags_stats():
     return _pico().F_STATS
+
+
+def test_long_path_many_rounds():
+    """A path needs l2 = (n-1)//2 synchronous rounds (pinned on small paths
+    against the Jacobi reference): far beyond the per-round records, still a
+    valid input, for every Index2core algorithm and PeelOne."""
+    for n in (5, 8, 31, 64):
+        rp, ci = synth.to_numpy(*synth.path(n))
+        assert oracle.jacobi_rounds(rp, ci)[1] == (n - 1) // 2
+    n = 140_001
+    rp, ci = synth.to_numpy(*synth.path(n))
+    for algo in ("histocore", "peelone", "cntcore"):
+        core, st, _ = _run(rp, ci, algo, 0, fs_cap=16)
+        assert (core == 1).all()
+        if algo != "peelone":
+            assert st.rounds == (n - 1) // 2
