@@ -17,8 +17,11 @@ LIB = os.path.join(PKG, "libpico.so")
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xcompiler", "-fvisibility=default",
+]
+LINK_FLAGS = [
+    "-shared",
     "-ldl",  # NCCL is loaded with dlopen by the sharded entry points
 ]
 
@@ -47,15 +50,30 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
+    then link the shared library."""
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     target = out or LIB
     if not force and out is None and not needs_build():
         return LIB
     tmp = target + f".tmp{os.getpid()}"
-    cmd = ([nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines]
-           + ["-I" + INCLUDE, "-I" + CSRC, "-o", tmp] + sources())
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    with tempfile.TemporaryDirectory(prefix="pico_build_") as d:
+        def compile_one(src):
+            obj = os.path.join(d, os.path.basename(src) + ".o")
+            cmd = ([nvcc()] + NVCC_FLAGS + ["-D" + x for x in defines]
+                   + ["-I" + INCLUDE, "-I" + CSRC, "-c", src, "-o", obj])
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.check_call(cmd)
+            return obj
+        srcs = sources()
+        with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+            objs = list(ex.map(compile_one, srcs))
+        cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a"] + LINK_FLAGS + ["-o", tmp] + objs
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
     os.replace(tmp, target)
     return target
 
