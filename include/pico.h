@@ -93,6 +93,13 @@ enum {
                               /* atomicMax(k) on overshoot                   */
     PICO_F_CLAMP_CAS = 1024u, /* PeelOne: CAS-loop atomicSub>=k (the literal */
                               /* single-transaction clamp of P:273)          */
+    PICO_F_DEBUG_INVARIANTS = 4096u, /* HistoCore: after the rounds, check on */
+                              /* the device that every histogram matches    */
+                              /* the final estimates (bins < core count     */
+                              /* neighbours of that estimate, the cap bin   */
+                              /* those at or above it) and that  */
+                              /* the estimates are an h-index fixed point   */
+                              /* (P:138-146); a violation -> PICO_EGRAPH    */
     PICO_F_PREFILTER = 2048u, /* HistoCore: degree-bucket row order + scan   */
                               /* prefix (cuts scanned arcs ~44%; measured    */
                               /* slower on B200, so opt-in)                  */

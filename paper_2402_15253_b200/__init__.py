@@ -15,7 +15,7 @@ import ctypes
 
 import numpy as np
 
-from ._lib import (ALGOS, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
+from ._lib import (ALGOS, F_DEBUG_INVARIANTS, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
                    F_RELABEL, F_STATS, F_TIMING, F_TINY_TILES, F_VALIDATE, PicoError, Stats, check, header_functions, load)
 
 __all__ = ["coreness", "coreness_host", "workspace_bytes", "DynamicCoreness", "PicoError", "Stats", "load",

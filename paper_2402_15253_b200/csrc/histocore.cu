@@ -937,6 +937,51 @@ __device__ void update_phase(const HcArgs &a, int t) {
 }
 
 // ---------------------------------------------------------------------------
+// PICO_F_DEBUG_INVARIANTS: one warp per vertex recounts its
+// neighbours' final estimates and compares them with its histogram -- bins
+// b < core[v] hold #{u : core[u] = b}, the cap bin #{u : core[u] >= core[v]}
+// -- and checks the h-index fixed point HINDEX(core(nbr v)) =
+// core[v]: the cap count is >= core[v] and the count of
+// neighbours at or above core[v] + 1 is < core[v] + 1.  Any violation sets
+// *bad.  Caps up to 1024 are checked bin by bin, larger ones by their cap
+// bin and fixed point only.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) hc_check_kernel(HcArgs a, int *bad) {
+    __shared__ int sh[8][1025];
+    const int wib = threadIdx.x >> 5, lane = lane_id();
+    int *cnt = sh[wib];
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long v = gw; v < a.n; v += nw) {
+        const long long r0 = a.rp[v], r1 = a.rp[v + 1];
+        const int c = a.core[v];
+        if (r1 == r0) {
+            if (c != 0 && lane == 0) atomicOr(bad, 1);
+            continue;
+        }
+        const int B = min(c, 1024);
+        for (int b = lane; b <= B; b += 32) cnt[b] = 0;
+        __syncwarp();
+        int above = 0, above1 = 0;
+        for (long long e = r0 + lane; e < r1; e += 32) {
+            const int cu = a.core[a.ci[e]];
+            above += cu >= c;
+            above1 += cu >= c + 1;
+            if (cu < c && cu <= B) atomicAdd(&cnt[cu], 1);
+        }
+        above = (int)warp_sum64(above);
+        above1 = (int)warp_sum64(above1);
+        __syncwarp();
+        bool ok = c >= 1 && above >= c && above1 < c + 1;              // the fixed point
+        ok = ok && a.histo[r0 - 1 + c] == above;                        // the cap bin
+        if (c <= 1024)
+            for (int b = 1 + lane; b < c; b += 32) ok = ok && a.histo[r0 - 1 + b] == cnt[b];
+        if (__any_sync(FULL, !ok) && lane == 0) atomicOr(bad, 2);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // UpdateHisto, pull direction (dense rounds), over the bucketed edge list:
 // for each v-range bucket in turn every warp streams a contiguous slice of
 // its (u, v) pairs; arc (u, v) applies the (v, u) bin move of a changed v
@@ -1624,6 +1669,16 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         }
     }
     if ((err = cudaGetLastError())) return err;
+    if ((flags & PICO_F_DEBUG_INVARIANTS) && n > 0) {
+        int *bad = (int *)a.F;  // free after init
+        int hbad = 0;
+        if ((err = cudaMemsetAsync(bad, 0, sizeof(int), s))) return err;
+        hc_check_kernel<<<sms * 8, 256, 0, s>>>(a, bad);
+        launches++;
+        if ((err = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s))) return err;
+        if ((err = cudaStreamSynchronize(s))) return err;
+        if (hbad) return cudaErrorAssert;  // capi: PICO_EGRAPH
+    }
     if (st) {
         st->rounds = (int64_t)rounds;
         st->kernel_count += launches;

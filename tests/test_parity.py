@@ -271,3 +271,18 @@ def test_long_path_many_rounds():
         assert (core == 1).all()
         if algo != "peelone":
             assert st.rounds == (n - 1) // 2
+
+
+def test_debug_invariants():
+    """PICO_F_DEBUG_INVARIANTS re-counts every vertex's
+    histogram against the final estimates and checks the h-index fixed point
+    on the device, for the default, push-only, pull-always (multi-bucket) and
+    host-loop schedules."""
+    pico = _pico()
+    graphs = [synth.to_numpy(*synth.CONFIGS[c].build()) for c in ("R12", "R14", "C1")]
+    graphs += [g for _, g in _fixture_graphs()]
+    for rp, ci in graphs:
+        ref = oracle.bz(rp, ci)
+        for fl in (0, pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS | pico.F_TINY_TILES, pico.F_HOST_LOOP):
+            core, _, _ = _run(rp, ci, "histocore", fl | pico.F_DEBUG_INVARIANTS)
+            assert np.array_equal(core, ref)
