@@ -1,5 +1,5 @@
 """bench.py --gpus N (N > 1, launched by torchrun): sharded HistoCore
-(SURVEY 8(e)).  One process per GPU, NCCL over NVLink/NVSwitch for the
+(SURVEY 8(e)), or sharded PeelOne with --algo peelone.  One process per GPU, NCCL over NVLink/NVSwitch for the
 exchange (torch.distributed), libpico kernels for every compute step.
 
 A step = one complete sharded coreness computation of the graph (shard
@@ -51,16 +51,32 @@ def bench_sharded(args):
         except Exception as e:  # no usable libnccl: the torch.distributed exchange (also GPU, also NCCL)
             exchange_note = f"torch.distributed (in-library NCCL unavailable: {e})"
 
+    peel = args.algo == "peelone"
+
     def run_once(rp_d, ci_d):
         if comm is not None:  # one library call; the exchange runs over NCCL inside libpico
-            r = sharded.coreness_sharded_nccl(rp_d, ci_d, n, m, vb, comm, flags=args.flags)
-            r.triples_exchanged = sum(r.frontier_sizes)
+            r = sharded.coreness_sharded_nccl(rp_d, ci_d, n, m, vb, comm, flags=args.flags, algo=1 if peel else 0)
+            if peel:
+                r.subrounds = r.rounds
+                r.exchanged = sum(r.frontier_sizes)
+            else:
+                r.exchanged = sum(r.frontier_sizes)
+            return r
+        if peel:
+            shard = sharded.DevicePeelShard(rp_d, ci_d, vb, n, args.flags)
+            try:
+                r = sharded.run_peel_shard(shard, ex, dev)
+            finally:
+                shard.close()
+            r.exchanged = sum(r.level_sizes)
             return r
         shard = sharded.DeviceShard(rp_d, ci_d, vb, n, args.flags)
         try:
-            return sharded.run_shard(shard, ex, dev)
+            r = sharded.run_shard(shard, ex, dev)
         finally:
             shard.close()
+        r.exchanged = r.triples_exchanged
+        return r
 
     def step():
         return run_once(rp_l, ci_l)
@@ -130,14 +146,24 @@ def bench_sharded(args):
 
     if rank == 0:
         peak, src = bench.hbm_peak()
-        launches = 12 + 4 * run.rounds
+        launches = (8 + 3 * run.subrounds + 3 * run.levels) if peel else 12 + 4 * run.rounds
+        if peel:
+            iters = {"peelone_levels": run.levels, "peelone_subrounds": run.subrounds, "kmax": run.kmax}
+            exch = {"frontier_ids_per_step": run.exchanged, "bytes_per_rank_per_step": 4 * run.exchanged,
+                    "collectives_per_step": run.subrounds + run.levels + 1, "partition": bounds}
+            par = (f"1-D vertex partition x{world} (per sub-round: all-gather of (|F|, kmin) and allgatherv of "
+                   "the frontier over NCCL: " + exchange_note + ")")
+        else:
+            iters = {"histocore_l2": run.rounds}
+            exch = {"triples_per_step": run.exchanged, "bytes_per_rank_per_step": 12 * run.exchanged,
+                    "partition": bounds}
+            par = f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL: " + exchange_note + ")"
         out = {
             "metric": bench.METRIC, "value": m / (ms * 1e-3), "unit": bench.UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": cfg.note, "config": args.config, "algo": "histocore-sharded", "n": n, "m": m,
-                       "parallelism": f"1-D vertex partition x{world} (allgatherv of changed triples over NCCL: "
-                                      + exchange_note + ")",
+            "config": {"workload": cfg.note, "config": args.config, "algo": f"{args.algo}-sharded", "n": n, "m": m,
+                       "parallelism": par,
                        "l2_flush": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
                          "traffic": None, "peak_source": src + f" x {world} GPUs",
@@ -148,9 +174,8 @@ def bench_sharded(args):
             "gpu_launches": launches * args.steps * world,
             "clocks": clk.summary() if clk else None,
             "parity": parity,
-            "iterations": {"histocore_l2": run.rounds},
-            "exchange": {"triples_per_step": run.triples_exchanged, "bytes_per_rank_per_step": 12 * run.triples_exchanged,
-                         "partition": bounds},
+            "iterations": iters,
+            "exchange": exch,
         }
         print(json.dumps(out), flush=True)
     dist.barrier()

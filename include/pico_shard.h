@@ -1,5 +1,6 @@
 /*
- * pico_shard.h -- C ABI of the sharded (multi-GPU) HistoCore of libpico.so.
+ * pico_shard.h -- C ABI of the sharded (multi-GPU) HistoCore and PeelOne of
+ * libpico.so.
  *
  * SURVEY 8(e); PAPER.md names multi-GPU as future work.  The graph
  * is split by a 1-D vertex partition: rank r owns the rows of the contiguous
@@ -73,6 +74,56 @@ int pico_shard_result(pico_shard_t h, int32_t *core_local);
 int pico_shard_destroy(pico_shard_t h);
 
 /* ------------------------------------------------------------------------
+ * Sharded PeelOne: the level-synchronous peel of Alg 4
+ * (clamp atomicSub>=k P:273; dynamic frontier P:342) over the same
+ * 1-D partition.  A level k is
+ *
+ *     pico_peel_shard_scan   -> this rank's F = {owned alive u : core[u] == k}
+ *     repeat:
+ *       all-gather of the counts; a global count of 0 ends the level
+ *       allgatherv of F (int32 GLOBAL ids, rank order)   (caller / NCCL)
+ *       pico_peel_shard_apply -> clamped decrements over the local CSC of
+ *                                every received v; owned u that reach k form
+ *                                this rank's next F (same level)
+ *
+ * Each call also returns kmin, a lower bound of the smallest estimate above
+ * k of this rank's alive vertices (INT32_MAX if none).  At the end of a level
+ * the next level is max(k + 1, min over ranks of kmin); the run ends when
+ * that minimum is INT32_MAX.  The first k comes from create's kmin.  Every
+ * sub-round is a BSP sub-round of the single-GPU PeelOne, so the coreness is
+ * bit-exact and the non-empty level and sub-round counts do not depend on the
+ * number of ranks.  No degree exchange is needed.
+ *
+ * Conventions as for pico_shard_*; frontier buffers are device int32 with
+ * cap >= nloc (an owned vertex enters F at most once per run), else
+ * PICO_EINVAL.  Call order: create, { scan, { apply }* }*, result, destroy.
+ * ---------------------------------------------------------------------- */
+typedef struct pico_peel_shard_s *pico_peel_shard_t;
+
+/* core = degree on the owned rows, alive list, local CSC.  *kmin <- smallest
+ * nonzero owned degree (INT32_MAX if every owned vertex is isolated).
+ * flags: PICO_F_TINY_TILES (tests), PICO_F_CLAMP_CAS, PICO_F_STATS. */
+int pico_peel_shard_create(const int64_t *rowptr_local, const int32_t *colidx_local, int64_t nloc,
+                           int64_t v_begin, int64_t n_global, uint32_t flags, pico_stream_t stream,
+                           pico_peel_shard_t *out, int32_t *kmin);
+
+/* Start level k (k > every earlier level): frontier[0..*count) <- this rank's
+ * owned vertices with core == k (global ids); *kmin as above. */
+int pico_peel_shard_scan(pico_peel_shard_t h, int32_t k, int32_t *frontier, int64_t cap, int64_t *count,
+                         int32_t *kmin);
+
+/* One sub-round: frontier_all (device int32 [total], every rank's F) ->
+ * clamped decrements of the owned neighbours; frontier[0..*count) <- the
+ * owned vertices that reached k (global ids); *kmin as above. */
+int pico_peel_shard_apply(pico_peel_shard_t h, const int32_t *frontier_all, int64_t total, int32_t *frontier,
+                          int64_t cap, int64_t *count, int32_t *kmin);
+
+/* core_local (device int32 [nloc]) <- coreness of the owned vertices. */
+int pico_peel_shard_result(pico_peel_shard_t h, int32_t *core_local);
+
+int pico_peel_shard_destroy(pico_peel_shard_t h);
+
+/* ------------------------------------------------------------------------
  * One-call sharded coreness with the exchange inside the library (NCCL over
  * NVLink/NVSwitch).  One process (or thread) per GPU.
  * libnccl.so.2 is loaded on first use (dlopen); if it cannot be loaded the
@@ -98,18 +149,21 @@ int pico_comm_size(pico_comm_t comm, int *nranks, int *rank);
  * (int32 GLOBAL ids) are DEVICE arrays of the owned rows; core_out_local
  * (device int32 [nloc]) receives their coreness.  m_global = undirected edges
  * of the whole graph (the local arc counts must sum to 2 m_global, else
- * PICO_EINVAL on every rank).  algo: PICO_ALGO_HISTOCORE (PeelOne is not
- * sharded: PICO_ENOTSUP).  Collective and blocking: every rank calls it with
- * its own range; the per-round exchange is an all-gather of the changed-triple
- * counts (the global convergence test) and a grouped-broadcast all-gatherv of
- * the (v, oldcore, core) triples, both on `stream`. */
+ * PICO_EINVAL on every rank).  algo: PICO_ALGO_HISTOCORE or PICO_ALGO_PEELONE
+ * (other algos: PICO_EINVAL).  Collective and blocking: every rank calls it
+ * with its own range.  HistoCore's per-round exchange is an all-gather of the
+ * changed-triple counts (the global convergence test) and a grouped-broadcast
+ * all-gatherv of the (v, oldcore, core) triples; PeelOne's per-sub-round
+ * exchange is an all-gather of (|F|, kmin) pairs and a grouped-broadcast
+ * all-gatherv of F (see pico_peel_shard_*); all on `stream`. */
 int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
                           int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
                           int32_t *core_out_local, pico_stream_t stream);
 
-/* Same with PICO_F_* schedule flags and optional stats (rounds = l2 and,
- * when stats->frontier_sizes is set, the GLOBAL |C_t| per round, identical
- * on every rank). */
+/* Same with PICO_F_* schedule flags and optional stats, identical on every
+ * rank.  HistoCore: rounds = l2 and, when stats->frontier_sizes is set, the
+ * GLOBAL |C_t| per round.  PeelOne: levels, subrounds, kmax and, in
+ * frontier_sizes, the vertices processed per non-empty level (global). */
 int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
                              int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
                              int32_t *core_out_local, pico_stream_t stream, uint32_t flags,

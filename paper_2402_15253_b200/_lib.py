@@ -133,7 +133,7 @@ def load(path: str | None = None):
 
 
 def _setup_shard(lib):
-    """Signatures of the sharded-HistoCore entry points (include/pico_shard.h)."""
+    """Signatures of the sharded HistoCore / PeelOne entry points (include/pico_shard.h)."""
     if not hasattr(lib, "pico_shard_create"):
         return
     vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint32
@@ -152,6 +152,17 @@ def _setup_shard(lib):
     lib.pico_shard_result.restype = i32
     lib.pico_shard_destroy.argtypes = [vp]
     lib.pico_shard_destroy.restype = i32
+    P32 = ctypes.POINTER(ctypes.c_int32)
+    lib.pico_peel_shard_create.argtypes = [vp, vp, i64, i64, i64, u32, vp, ctypes.POINTER(vp), P32]
+    lib.pico_peel_shard_create.restype = i32
+    lib.pico_peel_shard_scan.argtypes = [vp, i32, vp, i64, P64, P32]
+    lib.pico_peel_shard_scan.restype = i32
+    lib.pico_peel_shard_apply.argtypes = [vp, vp, i64, vp, i64, P64, P32]
+    lib.pico_peel_shard_apply.restype = i32
+    lib.pico_peel_shard_result.argtypes = [vp, vp]
+    lib.pico_peel_shard_result.restype = i32
+    lib.pico_peel_shard_destroy.argtypes = [vp]
+    lib.pico_peel_shard_destroy.restype = i32
     if hasattr(lib, "pico_coreness_sharded"):
         u8p = ctypes.POINTER(ctypes.c_uint8)
         lib.pico_comm_unique_id.argtypes = [u8p]

@@ -483,6 +483,78 @@ int pico_shard_destroy(pico_shard_t h) {
     return e ? cuda_fail(e, "shard destroy") : PICO_OK;
 }
 
+// sharded PeelOne steps
+struct pico_peel_shard_s {
+    PeelShard *impl;
+};
+
+static int peel_read(pico_peel_shard_t h, int64_t *count, int32_t *kmin) {
+    long long c = 0;
+    int km = 0;
+    cudaError_t e = pshard_read(h->impl, &c, &km);
+    if (e) return cuda_fail(e, "peel shard read");
+    if (count) *count = c;
+    if (kmin) *kmin = km;
+    return PICO_OK;
+}
+
+int pico_peel_shard_create(const int64_t *rowptr_local, const int32_t *colidx_local, int64_t nloc,
+                           int64_t v_begin, int64_t n_global, uint32_t flags, pico_stream_t stream,
+                           pico_peel_shard_t *out, int32_t *kmin) {
+    g_last_error.clear();
+    if (!out) return fail(PICO_EINVAL, "NULL output handle");
+    *out = nullptr;
+    if (nloc < 0 || v_begin < 0 || n_global <= 0 || v_begin + nloc > n_global)
+        return fail(PICO_EINVAL, "bad shard range [%lld, %lld) of %lld", (long long)v_begin,
+                    (long long)(v_begin + nloc), (long long)n_global);
+    if (n_global >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n_global needs 64-bit vertex ids");
+    if (!rowptr_local) return fail(PICO_EINVAL, "NULL rowptr_local");
+    DevInfo dev;
+    cudaError_t e = dev_info(&dev);
+    if (e) return cuda_fail(e, "device query");
+    PeelShard *impl = nullptr;
+    e = pshard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags,
+                      (cudaStream_t)stream, dev, &impl);
+    if (e) return cuda_fail(e, "peel shard create");
+    *out = new pico_peel_shard_s{impl};
+    return peel_read(*out, nullptr, kmin);
+}
+
+int pico_peel_shard_scan(pico_peel_shard_t h, int32_t k, int32_t *frontier, int64_t cap, int64_t *count,
+                         int32_t *kmin) {
+    g_last_error.clear();
+    if (!h || !count || !kmin || k < 1) return fail(PICO_EINVAL, "bad argument");
+    if (cap < pshard_nloc(h->impl) || (cap > 0 && !frontier)) return fail(PICO_EINVAL, "frontier cap < nloc");
+    cudaError_t e = pshard_scan(h->impl, k, frontier);
+    if (e) return cuda_fail(e, "peel shard scan");
+    return peel_read(h, count, kmin);
+}
+
+int pico_peel_shard_apply(pico_peel_shard_t h, const int32_t *frontier_all, int64_t total, int32_t *frontier,
+                          int64_t cap, int64_t *count, int32_t *kmin) {
+    g_last_error.clear();
+    if (!h || !count || !kmin || total < 0 || (total > 0 && !frontier_all)) return fail(PICO_EINVAL, "bad argument");
+    if (cap < pshard_nloc(h->impl) || (cap > 0 && !frontier)) return fail(PICO_EINVAL, "frontier cap < nloc");
+    cudaError_t e = pshard_apply(h->impl, frontier_all, total, frontier);
+    if (e) return cuda_fail(e, "peel shard apply");
+    return peel_read(h, count, kmin);
+}
+
+int pico_peel_shard_result(pico_peel_shard_t h, int32_t *core_local) {
+    g_last_error.clear();
+    if (!h) return fail(PICO_EINVAL, "NULL shard");
+    cudaError_t e = pshard_result(h->impl, core_local);
+    return e ? cuda_fail(e, "peel shard result") : PICO_OK;
+}
+
+int pico_peel_shard_destroy(pico_peel_shard_t h) {
+    g_last_error.clear();
+    if (!h) return PICO_OK;
+    cudaError_t e = pshard_destroy(h->impl);
+    delete h;
+    return e ? cuda_fail(e, "peel shard destroy") : PICO_OK;
+}
+
 }  // extern "C"
 
 // ===========================================================================
@@ -558,6 +630,85 @@ static int nccl_fail(ncclResult_t r, const char *where) {
     return fail(PICO_ENCCL, "%s: %s", where, nccl().GetErrorString ? nccl().GetErrorString(r) : "NCCL error");
 }
 
+// Sharded PeelOne level loop over NCCL (pico_peel_shard_* semantics): per
+// sub-round one all-gather of the (|F|, kmin) pairs straight from device
+// memory, one host read, and a grouped-broadcast all-gatherv of F.
+static int peel_rounds(pico_comm_t comm, PeelShard *ps, long long nloc, int *front, int *&all, size_t &all_cap,
+                       long long *cnt, int32_t *core_out_local, pico_stats_t *stats, cudaStream_t s) {
+    NcclApi &N = nccl();
+    const int P = comm->nranks, me = comm->rank;
+    std::vector<long long> hp(2 * P), off(P + 1, 0);
+    const long long *odev = pshard_out(ps);
+    cudaError_t e;
+    ncclResult_t nr, ne;
+    long long levels = 0, subrounds = 0;
+    int kmax = 0;
+    // (count, kmin) of every rank -> host; returns the global total and min
+    auto gather = [&](long long *total, int *kmin) -> int {
+        if ((nr = N.AllGather(odev, cnt + 2, 2, ncclInt64, comm->c, s)) != ncclSuccess)
+            return nccl_fail(nr, "allgather counts");
+        if ((e = cudaMemcpyAsync(hp.data(), cnt + 2, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost, s)) ||
+            (e = cudaStreamSynchronize(s)))
+            return cuda_fail(e, "counts");
+        long long t = 0, km = INT_MAX;
+        for (int r = 0; r < P; r++) {
+            off[r] = t;
+            t += hp[2 * r];
+            km = std::min(km, hp[2 * r + 1]);
+        }
+        off[P] = t;
+        *total = t;
+        *kmin = (int)km;
+        return PICO_OK;
+    };
+    long long total = 0;
+    int kmin = INT_MAX, rc;
+    if ((rc = gather(&total, &kmin)) != PICO_OK) return rc;
+    int k = 0;
+    while (kmin != INT_MAX) {
+        k = std::max(k + 1, kmin);
+        if ((e = pshard_scan(ps, k, front))) return cuda_fail(e, "peel scan");
+        long long processed = 0;
+        for (;;) {
+            if ((rc = gather(&total, &kmin)) != PICO_OK) return rc;
+            if (total == 0) break;  // the level is done on every rank
+            processed += total;
+            subrounds++;
+            if ((size_t)total > all_cap) {
+                if (all) cudaFreeAsync(all, s);
+                all_cap = (size_t)total + (size_t)total / 4;
+                if ((e = cudaMallocAsync((void **)&all, sizeof(int) * all_cap, s))) {
+                    all = nullptr;
+                    return cuda_fail(e, "alloc");
+                }
+            }
+            if ((nr = N.GroupStart()) != ncclSuccess) return nccl_fail(nr, "group");
+            for (int r = 0; r < P && nr == ncclSuccess; r++) {
+                long long c = off[r + 1] - off[r];
+                if (c > 0)
+                    nr = N.Broadcast(r == me ? (const void *)front : (const void *)(all + off[r]), all + off[r],
+                                     (size_t)c, ncclInt32, r, comm->c, s);
+            }
+            ne = N.GroupEnd();
+            if (nr != ncclSuccess || ne != ncclSuccess) return nccl_fail(nr != ncclSuccess ? nr : ne, "allgatherv F");
+            if ((e = pshard_apply(ps, all, total, front))) return cuda_fail(e, "peel apply");
+        }
+        if (processed) {
+            if (stats && stats->frontier_sizes && levels < stats->frontier_sizes_cap)
+                stats->frontier_sizes[levels] = processed;
+            levels++;
+            kmax = k;
+        }
+    }
+    if (stats) {
+        stats->levels = levels;
+        stats->subrounds = subrounds;
+        stats->kmax = kmax;
+    }
+    if (nloc > 0 && (e = pshard_result(ps, core_out_local))) return cuda_fail(e, "shard result");
+    return PICO_OK;
+}
+
 extern "C" {
 
 int pico_comm_unique_id(uint8_t id[128]) {
@@ -609,8 +760,8 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
     g_last_error.clear();
     reset_stats(stats);
     if (!comm) return fail(PICO_EINVAL, "NULL comm");
-    if (algo == PICO_ALGO_PEELONE) return fail(PICO_ENOTSUP, "PeelOne is not sharded (replicas only)");
-    if (algo != PICO_ALGO_HISTOCORE) return fail(PICO_EINVAL, "unknown algo %d", algo);
+    if (algo != PICO_ALGO_HISTOCORE && algo != PICO_ALGO_PEELONE)
+        return fail(PICO_EINVAL, "algo %d is not sharded", algo);
     if (v_begin < 0 || v_end < v_begin || v_end > n_global || n_global <= 0 || m_global < 0)
         return fail(PICO_EINVAL, "bad range [%lld, %lld) of %lld", (long long)v_begin, (long long)v_end,
                     (long long)n_global);
@@ -625,7 +776,12 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
     if (e) return cuda_fail(e, "device query");
 
     Shard *sh = nullptr;
-    e = shard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags, s, dev, &sh);
+    PeelShard *ps = nullptr;
+    const bool peel = algo == PICO_ALGO_PEELONE;
+    if (peel)
+        e = pshard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags, s, dev, &ps);
+    else
+        e = shard_create((const long long *)rowptr_local, colidx_local, nloc, v_begin, n_global, flags, s, dev, &sh);
     if (e) return cuda_fail(e, "shard create");
     // device scratch: meta [3 + 3P] int64, counts [1 + P] int64, degrees, triples
     long long *meta = nullptr, *cnt = nullptr;
@@ -639,7 +795,7 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
     auto bail_nccl = [&](ncclResult_t r, const char *w) { rc = nccl_fail(r, w); };
     do {
         if ((e = cudaMallocAsync((void **)&meta, sizeof(long long) * (3 + 3 * P), s))) { bail_cuda(e, "alloc"); break; }
-        if ((e = cudaMallocAsync((void **)&cnt, sizeof(long long) * (1 + P), s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = cudaMallocAsync((void **)&cnt, sizeof(long long) * (2 + 2 * P), s))) { bail_cuda(e, "alloc"); break; }
         if ((e = cudaMallocAsync((void **)&deg_g, sizeof(int) * (size_t)n_global, s))) { bail_cuda(e, "alloc"); break; }
         if ((e = cudaMallocAsync((void **)&trip, sizeof(int) * 3 * (size_t)std::max(nloc, 1ll), s))) {
             bail_cuda(e, "alloc");
@@ -661,6 +817,10 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
         }
         if (!tiled) { rc = fail(PICO_EINVAL, "rank ranges do not tile [0, n_global) in rank order"); break; }
         if (arcs != 2 * m_global) { rc = fail(PICO_EINVAL, "local arcs sum to %lld, not 2m = %lld", arcs, 2 * (long long)m_global); break; }
+        if (peel) {
+            rc = peel_rounds(comm, ps, nloc, trip, all, all_cap, cnt, core_out_local, stats, s);
+            break;
+        }
         // degrees: all-gatherv into deg_global
         if ((e = shard_degrees(sh, deg_g + v_begin))) { bail_cuda(e, "shard degrees"); break; }
         if ((nr = N.GroupStart()) != ncclSuccess) { bail_nccl(nr, "group"); break; }
@@ -706,7 +866,7 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
         if (stats) stats->rounds = rounds;
         if (nloc > 0 && (e = shard_result(sh, core_out_local))) { bail_cuda(e, "shard result"); break; }
     } while (false);
-    cudaError_t ed = shard_destroy(sh);
+    cudaError_t ed = peel ? pshard_destroy(ps) : shard_destroy(sh);
     for (void *ptr : {(void *)meta, (void *)cnt, (void *)deg_g, (void *)trip, (void *)all})
         if (ptr) cudaFreeAsync(ptr, s);
     cudaError_t es = cudaStreamSynchronize(s);

@@ -60,6 +60,20 @@ cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long
 cudaError_t shard_result(Shard *h, int *core_out);
 cudaError_t shard_destroy(Shard *h);
 
+// sharded PeelOne (shard_peel.cu): each call publishes (|F| of this rank,
+// next-level bound) as two int64 on the device (pshard_out)
+struct PeelShard;
+cudaError_t pshard_create(const long long *rp, const int *ci, long long nloc, long long vb, long long ng,
+                          uint32_t flags, cudaStream_t s, const DevInfo &dev, PeelShard **out);
+const long long *pshard_out(PeelShard *h);
+long long pshard_nloc(PeelShard *h);
+cudaError_t pshard_scan(PeelShard *h, int k, int *front);
+cudaError_t pshard_apply(PeelShard *h, const int *all, long long total, int *front);
+cudaError_t pshard_read(PeelShard *h, long long *count, int *kmin);
+cudaError_t pshard_counters(PeelShard *h, long long *arcs_scanned, long long *guarded);
+cudaError_t pshard_result(PeelShard *h, int *core_out);
+cudaError_t pshard_destroy(PeelShard *h);
+
 // decremental HistoCore (histocore.cu)
 struct Dyn;
 cudaError_t dyn_create(const long long *rp, const int *ci, long long n, long long arcs, uint32_t flags,

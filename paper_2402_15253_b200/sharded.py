@@ -1,5 +1,5 @@
-"""Sharded (multi-GPU) HistoCore driver -- SURVEY 8(e); PAPER.md P:894 lists
-multi-GPU as future work.
+"""Sharded (multi-GPU) HistoCore and PeelOne drivers -- SURVEY 8(e), 8(f)
+NEXT-1; PAPER.md P:894 lists multi-GPU as future work.
 
 The compute of every step runs in libpico's kernels (include/pico_shard.h).
 This module is the plumbing between the steps:
@@ -7,7 +7,8 @@ This module is the plumbing between the steps:
   * the exchange: all-gather of the per-rank counts (which is also the global
     convergence test: a round with a global count of 0 ends the run) and an
     all-gather(v) of the changed (v, oldcore, core) triples;
-  * the round loop.
+  * the round loop (HistoCore) / the level and sub-round loops (PeelOne:
+    an all-gather of (|F|, kmin) pairs and an all-gatherv of F per sub-round).
 
 Exchanges:
   * TorchDistExchange -- torch.distributed (NCCL over NVLink/NVSwitch on B200,
@@ -85,6 +86,15 @@ class TorchDistExchange:
         if all(c == mx for c in counts):
             return out
         return torch.cat([out[r * mx:r * mx + c] for r, c in enumerate(counts)])
+
+    def allgather_pairs(self, a: int, b: int, device) -> list[tuple[int, int]]:
+        """Every rank's (a, b), in rank order (one collective)."""
+        import torch
+        t = torch.tensor([a, b], dtype=torch.int64, device=device)
+        out = torch.empty(2 * self.world, dtype=torch.int64, device=device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        v = out.tolist()
+        return [(v[2 * r], v[2 * r + 1]) for r in range(self.world)]
 
     def max_over_ranks(self, x: float, device) -> float:
         import torch
@@ -210,6 +220,158 @@ def coreness_sharded(rowptr, colidx, group=None, flags: int = 0) -> ShardRun:
 
 
 # ---------------------------------------------------------------------------
+# sharded PeelOne (pico_peel_shard_*)
+# ---------------------------------------------------------------------------
+INT32_MAX = 2**31 - 1
+
+
+class DevicePeelShard:
+    """The rank's PeelOne state in libpico (owned rows [vb, vb + nloc))."""
+
+    def __init__(self, rowptr_local, colidx_local, vb: int, n_global: int, flags: int = 0, stream=None):
+        import torch
+        self.lib = load()
+        self.dev = rowptr_local.device
+        self.rp, self.ci = rowptr_local, colidx_local
+        self.nloc = rowptr_local.numel() - 1
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        h, km = ctypes.c_void_p(), ctypes.c_int32()
+        check(self.lib.pico_peel_shard_create(self.rp.data_ptr(), self.ci.data_ptr() if self.ci.numel() else None,
+                                              self.nloc, vb, n_global, flags,
+                                              ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h),
+                                              ctypes.byref(km)))
+        self.h, self.kmin0 = h, km.value
+        self.front = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=self.dev)
+
+    def scan(self, k: int):
+        c, km = ctypes.c_int64(), ctypes.c_int32()
+        check(self.lib.pico_peel_shard_scan(self.h, k, self.front.data_ptr(), self.front.numel(), ctypes.byref(c),
+                                            ctypes.byref(km)))
+        return self.front, c.value, km.value
+
+    def apply(self, frontier_all, total: int):
+        c, km = ctypes.c_int64(), ctypes.c_int32()
+        check(self.lib.pico_peel_shard_apply(self.h, frontier_all.data_ptr() if total else None, total,
+                                             self.front.data_ptr(), self.front.numel(), ctypes.byref(c),
+                                             ctypes.byref(km)))
+        return self.front, c.value, km.value
+
+    def result(self):
+        import torch
+        out = torch.empty(max(self.nloc, 1), dtype=torch.int32, device=self.dev)
+        check(self.lib.pico_peel_shard_result(self.h, out.data_ptr()))
+        return out[:self.nloc]
+
+    def close(self):
+        if self.h:
+            check(self.lib.pico_peel_shard_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class PeelRun:
+    core_local: object
+    levels: int = 0
+    subrounds: int = 0
+    kmax: int = 0
+    level_sizes: list = field(default_factory=list)  # vertices processed per non-empty level
+
+
+def run_peel_shard(shard, exchange, device) -> PeelRun:
+    """The sharded PeelOne loop for one rank (pico_peel_shard_* protocol).
+
+    shard: DevicePeelShard (or any object with kmin0 / scan / apply / result);
+    exchange: TorchDistExchange (or any object with allgather_pairs /
+    allgatherv).  Per sub-round: an all-gather of (|F|, kmin) -- a global
+    |F| of 0 ends the level, and the minimum kmin is the next level's bound --
+    and an all-gatherv of F."""
+    run = PeelRun(core_local=None)
+    kmin = min(b for _, b in exchange.allgather_pairs(0, shard.kmin0, device))
+    k = 0
+    while kmin != INT32_MAX:
+        k = max(k + 1, kmin)
+        front, cnt, km = shard.scan(k)
+        processed = 0
+        while True:
+            pairs = exchange.allgather_pairs(cnt, km, device)
+            counts = [c for c, _ in pairs]
+            kmin = min(b for _, b in pairs)
+            total = sum(counts)
+            if total == 0:
+                break
+            processed += total
+            run.subrounds += 1
+            allf = exchange.allgatherv(front, counts)
+            front, cnt, km = shard.apply(allf, total)
+        if processed:
+            run.levels += 1
+            run.kmax = k
+            run.level_sizes.append(processed)
+    run.core_local = shard.result()
+    return run
+
+
+def coreness_sharded_peel(rowptr, colidx, group=None, flags: int = 0) -> PeelRun:
+    """Sharded PeelOne of the full graph over a torch.distributed group (one
+    process per GPU; only this rank's rows are used)."""
+    ex = TorchDistExchange(group)
+    bounds = partition(rowptr, ex.world)
+    vb, ve = bounds[ex.rank], bounds[ex.rank + 1]
+    rp_l, ci_l = local_rows(rowptr, colidx, vb, ve)
+    shard = DevicePeelShard(rp_l, ci_l, vb, rowptr.numel() - 1, flags)
+    try:
+        run = run_peel_shard(shard, ex, rowptr.device)
+    finally:
+        shard.close()
+    run.v_begin, run.v_end = vb, ve
+    return run
+
+
+def coreness_loopback_peel(rowptr, colidx, nparts: int, flags: int = 0) -> PeelRun:
+    """Sharded PeelOne with P logical shards on one GPU; the all-gathers are
+    device concatenations.  Returns a PeelRun over all vertices."""
+    import torch
+    n = rowptr.numel() - 1
+    bounds = partition(rowptr, nparts)
+    shards = []
+    run = PeelRun(core_local=None)
+    try:
+        for r in range(nparts):
+            rp_l, ci_l = local_rows(rowptr, colidx, bounds[r], bounds[r + 1])
+            shards.append(DevicePeelShard(rp_l, ci_l, bounds[r], n, flags))
+        kmin = min(s.kmin0 for s in shards)
+        k = 0
+        while kmin != INT32_MAX:
+            k = max(k + 1, kmin)
+            outs = [s.scan(k) for s in shards]
+            processed = 0
+            while True:
+                kmin = min(km for _, _, km in outs)
+                total = sum(c for _, c, _ in outs)
+                if total == 0:
+                    break
+                processed += total
+                run.subrounds += 1
+                allf = torch.cat([f[:c] for f, c, _ in outs])
+                outs = [s.apply(allf, total) for s in shards]
+            if processed:
+                run.levels += 1
+                run.kmax = k
+                run.level_sizes.append(processed)
+        run.core_local = torch.cat([s.result() for s in shards])
+    finally:
+        for s in shards:
+            s.close()
+    return run
+
+
+# ---------------------------------------------------------------------------
 # one-call path: the exchange inside libpico over NCCL (pico_coreness_sharded)
 # ---------------------------------------------------------------------------
 class NcclComm:
@@ -251,9 +413,11 @@ class NcclComm:
 
 def coreness_sharded_nccl(rowptr_local, colidx_local, n_global: int, m_global: int, v_begin: int,
                           comm: NcclComm, flags: int = 0, algo: int = 0, stream=None, frontier_cap: int = 1 << 16):
-    """Sharded HistoCore of this rank's rows [v_begin, v_begin + nloc) in ONE
-    library call (pico_coreness_sharded_ex): the per-round exchange runs over
-    NCCL inside libpico.  Returns a ShardRun (core_local, rounds, global |C_t|)."""
+    """Sharded HistoCore (algo 0) or PeelOne (algo 1) of this rank's rows
+    [v_begin, v_begin + nloc) in ONE library call (pico_coreness_sharded_ex):
+    the exchange runs over NCCL inside libpico.  Returns a ShardRun (core_local,
+    rounds, global |C_t|; for PeelOne rounds = sub-rounds, frontier_sizes = the
+    vertices processed per non-empty level, plus .levels and .kmax)."""
     import torch
     from ._lib import Stats
     lib = load()
@@ -269,6 +433,11 @@ def coreness_sharded_nccl(rowptr_local, colidx_local, n_global: int, m_global: i
                                        colidx_local.data_ptr() if colidx_local.numel() else None, n_global, m_global,
                                        v_begin, v_begin + nloc, algo, out.data_ptr() if nloc else None,
                                        ctypes.c_void_p(stream.cuda_stream), flags, ctypes.byref(st)))
+    if algo == 1:
+        run = ShardRun(core_local=out[:nloc], rounds=int(st.subrounds))
+        run.levels, run.kmax = int(st.levels), int(st.kmax)
+        run.frontier_sizes = [int(x) for x in fs[:run.levels]]
+        return run
     run = ShardRun(core_local=out[:nloc], rounds=int(st.rounds))
     run.frontier_sizes = [int(x) for x in fs[:run.rounds]]
     return run

@@ -76,3 +76,22 @@ def test_full_size_sharded_loopback(parts):
     assert rounds == st.rounds and sizes == [int(x) for x in fs[:st.rounds]]
     del rp, ci
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("parts", [2, 4])
+def test_full_size_sharded_peel_loopback(parts):
+    """Sharded PeelOne on the full C2 graph, P logical
+    shards on one GPU, against the BZ oracle; non-empty levels, sub-rounds and
+    k_max equal the single-GPU PeelOne's."""
+    import torch
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import sharded
+    rp, ci = _graph("C2")
+    ref = oracle.bz(*synth.to_numpy(rp, ci))
+    run = sharded.coreness_loopback_peel(rp, ci, parts)
+    assert np.array_equal(run.core_local.cpu().numpy(), ref)
+    st = pico.Stats()
+    pico.coreness(rp, ci, algo="peelone", stats=st)
+    assert (run.levels, run.subrounds, run.kmax) == (st.levels, st.subrounds, st.kmax)
+    del rp, ci
+    torch.cuda.empty_cache()

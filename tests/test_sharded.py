@@ -145,6 +145,94 @@ def test_gloo_world2_protocol(cfg):
     assert rounds == l2 and sizes == fs
 
 
+class NumpyPeelShard:
+    """Owned vertices [vb, ve): the level-synchronous peel on owned residual
+    degrees, decremented only through exchanged frontier vertices (the
+    pico_peel_shard_* protocol on the host)."""
+
+    def __init__(self, rp_l, ci_l, vb, n_global):
+        self.vb, self.nloc = vb, rp_l.size - 1
+        self.core = np.diff(rp_l).astype(np.int64)
+        self.csc = {}
+        for u in range(self.nloc):
+            for v in ci_l[rp_l[u]:rp_l[u + 1]]:
+                self.csc.setdefault(int(v), []).append(u)
+        alive = self.core[self.core > 0]
+        self.kmin0 = int(alive.min()) if alive.size else sharded.INT32_MAX
+        self.k = 0
+        self.bound = sharded.INT32_MAX
+
+    def scan(self, k):
+        self.k = k
+        keep = self.core > k
+        self.bound = int(self.core[keep].min()) if keep.any() else sharded.INT32_MAX
+        f = np.flatnonzero(self.core == k) + self.vb
+        return torch.from_numpy(f.astype(np.int32)), f.size, self.bound
+
+    def apply(self, allf, total):
+        k, nxt = self.k, []
+        for v in allf.numpy()[:total]:
+            for u in self.csc.get(int(v), []):
+                if self.core[u] > k:  # guard, then the clamped decrement (P:273)
+                    self.core[u] -= 1
+                    if self.core[u] == k:
+                        nxt.append(u + self.vb)
+                    else:
+                        self.bound = min(self.bound, int(self.core[u]))
+        f = np.array(nxt, dtype=np.int32)
+        return torch.from_numpy(f), f.size, self.bound
+
+    def result(self):
+        return torch.from_numpy(self.core.astype(np.int32))
+
+
+def _gloo_peel_worker(rank, world, port, cfg, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rp, ci = synth.CONFIGS[cfg].build() if cfg in synth.CONFIGS else synth.g1()
+        rpn, cin = synth.to_numpy(rp, ci)
+        ex = sharded.TorchDistExchange()
+        b = sharded.partition(rpn, world)
+        rl, cl = sharded.local_rows(rp, ci, b[rank], b[rank + 1])
+        shard = NumpyPeelShard(rl.numpy(), cl.numpy(), b[rank], rpn.size - 1)
+        run = sharded.run_peel_shard(shard, ex, torch.device("cpu"))
+        counts = ex.allgather_counts(run.core_local.numel(), torch.device("cpu"))
+        core = ex.allgatherv(run.core_local, counts)
+        if rank == 0:
+            out.put((core.numpy().tolist(), run.levels, run.subrounds, run.kmax, run.level_sizes))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", ["G1", "R12"])
+def test_gloo_world2_peel_protocol(cfg):
+    """world_size 2 over gloo: the sharded PeelOne protocol ((|F|, kmin)
+    all-gather = level test and next-level bound, F all-gatherv) yields the
+    oracle coreness and the level-synchronous reference's level / sub-round
+    counts."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_peel_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    core, levels, subrounds, kmax, sizes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rp, ci = synth.to_numpy(*(synth.CONFIGS[cfg].build() if cfg in synth.CONFIGS else synth.g1()))
+    ref = oracle.bz(rp, ci)
+    assert core == ref.tolist()
+    _, km, lv, sr = oracle.peel_levels(rp, ci)
+    assert (levels, subrounds, kmax) == (lv, sr, km)
+    nz = ref[ref > 0]
+    assert sizes == [int((nz == c).sum()) for c in np.unique(nz)]
+
+
 def test_shard_capi_argument_errors():
     import ctypes
     import paper_2402_15253_b200 as pico
@@ -158,6 +246,11 @@ def test_shard_capi_argument_errors():
     assert lib.pico_shard_create(rp.ctypes.data, None, -1, 0, 4, 0, None, ctypes.byref(h)) == 1
     assert lib.pico_shard_create(rp.ctypes.data, None, 2, 0, 4, 0, None, None) == 1
     assert lib.pico_shard_destroy(None) == 0
+    km = ctypes.c_int32()
+    assert lib.pico_peel_shard_create(rp.ctypes.data, None, 2, 5, 4, 0, None, ctypes.byref(h), ctypes.byref(km)) == 1
+    assert lib.pico_peel_shard_create(rp.ctypes.data, None, 2, 0, 4, 0, None, None, ctypes.byref(km)) == 1
+    assert lib.pico_peel_shard_scan(None, 1, None, 0, None, None) == 1
+    assert lib.pico_peel_shard_destroy(None) == 0
 
 
 # ---------------------------------------------------------------- GPU
@@ -206,6 +299,41 @@ def test_loopback_c1():
             assert np.array_equal(core.cpu().numpy(), ref) and rounds == l2 and sizes == fs
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_loopback_peel_parity(parts):
+    """Sharded PeelOne (P logical shards, device concatenation as the
+    exchange): bit-exact coreness, and the non-empty levels, BSP sub-rounds,
+    k_max and per-level sizes of the single-GPU PeelOne / level-synchronous
+    reference, for every P."""
+    import paper_2402_15253_b200 as pico
+    dev = torch.device("cuda:0")
+    for name, (rp, ci) in _graphs():
+        ref = oracle.bz(rp, ci)
+        _, km, lv, sr = oracle.peel_levels(rp, ci)
+        nz = ref[ref > 0]
+        per_level = [int((nz == c).sum()) for c in np.unique(nz)]
+        for fl in (0, pico.F_TINY_TILES, pico.F_CLAMP_CAS | pico.F_STATS):
+            run = sharded.coreness_loopback_peel(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev),
+                                                 parts, fl)
+            got = run.core_local.cpu().numpy()
+            assert np.array_equal(got, ref), (name, parts, fl, np.flatnonzero(got != ref)[:5])
+            assert (run.levels, run.subrounds, run.kmax) == (lv, sr, km), (name, parts, fl)
+            assert run.level_sizes == per_level
+
+
+@pytest.mark.gpu
+def test_loopback_peel_c1():
+    rp, ci = synth.to_numpy(*synth.CONFIGS["C1"].build())
+    dev = torch.device("cuda:0")
+    ref = oracle.bz(rp, ci)
+    _, km, lv, sr = oracle.peel_levels(rp, ci)
+    for parts in (2, 8):
+        run = sharded.coreness_loopback_peel(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), parts)
+        assert np.array_equal(run.core_local.cpu().numpy(), ref)
+        assert (run.levels, run.subrounds, run.kmax) == (lv, sr, km)
+
+
 # ------------------------------------------------ one-call NCCL path (C ABI)
 @pytest.mark.gpu
 def test_sharded_abi_single_rank_nccl():
@@ -231,12 +359,19 @@ def test_sharded_abi_single_rank_nccl():
         lib = pico.load()
         out = torch.empty(n, dtype=torch.int32, device=dev)
         s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        # ranges must tile [0, n_global); arcs must sum to 2m; PeelOne is not sharded
+        # ranges must tile [0, n_global); arcs must sum to 2m; only HistoCore / PeelOne shard
         assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n + 5, m, 0, n, 0,
                                          out.data_ptr(), s) == 1
         assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n, m + 1, 0, n, 0,
                                          out.data_ptr(), s) == 1
-        assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n, m, 0, n, 1,
-                                         out.data_ptr(), s) == 2
+        assert lib.pico_coreness_sharded(comm.h, rp.data_ptr(), ci.data_ptr(), n, m, 0, n, 3,
+                                         out.data_ptr(), s) == 1
+        # sharded PeelOne through the same entry point
+        _, km, lv, sr = oracle.peel_levels(rp_np, ci_np)
+        for fl in (0, pico.F_TINY_TILES):
+            run = sharded.coreness_sharded_nccl(rp, ci, n, m, 0, comm, flags=fl, algo=1)
+            torch.cuda.synchronize()
+            assert np.array_equal(run.core_local.cpu().numpy(), ref)
+            assert (run.levels, run.rounds, run.kmax) == (lv, sr, km)
     finally:
         comm.close()
