@@ -34,6 +34,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef PICO_PO_PER
+#define PICO_PO_PER 2  // resident CTAs per SM of the persistent level kernel
+#endif
+#ifndef PICO_PO_MINB
+#define PICO_PO_MINB 1
+#endif
+
 namespace pico {
 
 struct PoArgs {
@@ -221,7 +228,7 @@ __global__ void po_init_kernel(PoArgs a) {
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
+__global__ void __launch_bounds__(512, PICO_PO_MINB) po_levels_kernel(PoArgs a) {
     constexpr bool CLAMP_SUB = MODE == 1;
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
@@ -389,7 +396,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     } else {
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, po_levels_kernel<MODE, STATS>, 512, 0);
-        int per = std::max(1, std::min(occ, 2));
+        int per = std::max(1, std::min(occ, PICO_PO_PER));
         void *args[] = {&a};
         err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<MODE, STATS>, sms * per, 512,
                                           args, 0, s);
