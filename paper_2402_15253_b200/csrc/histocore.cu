@@ -424,12 +424,19 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
 // the 2-byte one, so that only one shadow array competes for the L2 at a time
 // (RMAT-26: 31.6 -> 29.1 ms; on C2, whose shadows fit the L2 anyway, the
 // second launch costs more than it saves)
+// shared bins per warp: the rows of the PART 1 launch have d <= 255, so that
+// launch needs 256 bins per warp instead of b_max + 1 (8 KB per CTA instead of
+// 64 KB: the occupancy is set by registers, not by shared memory)
+template <int PART>
+__host__ __device__ constexpr int init_warp_stride(int b_max) {
+    return PART == 1 ? (b_max < (int)SAT8 ? b_max : (int)SAT8) + 1 : b_max + 1;
+}
 template <bool STATS, int PART>
 __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
     extern __shared__ int sh[];
     const int wib = threadIdx.x >> 5;
     const int lane = lane_id();
-    int *bins = sh + wib * (a.tn.b_max + 1);
+    int *bins = sh + wib * init_warp_stride<PART>(a.tn.b_max);
     const long long nB = (long long)bcast_u64(&a.ctl->nB);
     const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
@@ -1552,12 +1559,15 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
         int occB = 0, occC = 0;
         if (hc_init_split(n)) {
+            size_t smB1 = sizeof(int) * (size_t)init_warp_stride<1>(tn.b_max) * 8;
+            int occB1 = 0;
             cudaFuncSetAttribute(hc_init_warp_kernel<STATS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smB);
+                                 (int)smB1);
             cudaFuncSetAttribute(hc_init_warp_kernel<STATS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smB);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS, 1>, 256, smB);
-            hc_init_warp_kernel<STATS, 1><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB1, hc_init_warp_kernel<STATS, 1>, 256, smB1);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<STATS, 2>, 256, smB);
+            hc_init_warp_kernel<STATS, 1><<<sms * std::max(1, occB1), 256, smB1, s>>>(a);
             hc_init_warp_kernel<STATS, 2><<<sms * std::max(1, occB), 256, smB, s>>>(a);
             launches++;
         } else {
@@ -2089,10 +2099,13 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         size_t smB = sizeof(int) * (size_t)(tn.b_max + 1) * 8;
         int occB = 0, occC = 0;
         if (hc_init_split(h->ng)) {  // the gathered shadows are global-size on a shard
-            cudaFuncSetAttribute(hc_init_warp_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            size_t smB1 = sizeof(int) * (size_t)init_warp_stride<1>(tn.b_max) * 8;
+            int occB1 = 0;
+            cudaFuncSetAttribute(hc_init_warp_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB1);
             cudaFuncSetAttribute(hc_init_warp_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false, 1>, 256, smB);
-            hc_init_warp_kernel<false, 1><<<sms * std::max(1, occB), 256, smB, s>>>(a);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB1, hc_init_warp_kernel<false, 1>, 256, smB1);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, hc_init_warp_kernel<false, 2>, 256, smB);
+            hc_init_warp_kernel<false, 1><<<sms * std::max(1, occB1), 256, smB1, s>>>(a);
             hc_init_warp_kernel<false, 2><<<sms * std::max(1, occB), 256, smB, s>>>(a);
         } else {
             cudaFuncSetAttribute(hc_init_warp_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
