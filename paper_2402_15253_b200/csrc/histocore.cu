@@ -100,6 +100,7 @@ struct HcArgs {
     shadow_t *c8;          // [n]  min(deg, 255): degree shadow for rows with deg <= 255
     unsigned short *c16;   // [n]  min(deg, 65535): degree shadow for longer rows
     unsigned *rec;         // [n]  estimate record (new16 | old16 << 16)
+    unsigned short *e16;   // [n]  min(core, 65535): the estimate alone (push-round gathers)
     int *oldc;             // [n]
     int *histo;            // [2m]
     int *F;                // [n]  frontier list; init: hub fallback list
@@ -641,6 +642,7 @@ __global__ void hc_shadow_kernel(HcArgs a) {
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += nthreads) {
         int k = a.core[v], d = a.oldc[v];
         a.rec[v] = pack_rec(k, d);
+        a.e16[v] = (unsigned short)min(k, (int)RSAT);
     }
 }
 
@@ -860,6 +862,9 @@ __device__ __forceinline__ void arc_fetch(ArcStep<U> &st, int j0, int total, int
 // concatenated arcs U*32 at a time (owner lane by a 5-step shuffle binary
 // search), U arcs in flight per lane, no returning atomics.
 // ---------------------------------------------------------------------------
+#ifndef PICO_PUSH_E16
+#define PICO_PUSH_E16 1  // push gathers read the 2-byte estimate array, not the 4-byte record
+#endif
 template <bool STATS>
 __device__ void update_phase(const HcArgs &a, int t) {
     const int lane = lane_id();
@@ -912,7 +917,12 @@ __device__ void update_phase(const HcArgs &a, int t) {
             int cu[UA];
             unsigned rr[UA];
 #pragma unroll
-            for (int q = 0; q < UA; q++) rr[q] = cur.v[q] >= 0 ? ld_rec(a.rec + cur.v[q], hot) : 0u;
+            for (int q = 0; q < UA; q++)
+#if PICO_PUSH_E16
+                rr[q] = cur.v[q] >= 0 ? (unsigned)__ldcg(a.e16 + cur.v[q]) : 0u;
+#else
+                rr[q] = cur.v[q] >= 0 ? ld_rec(a.rec + cur.v[q], hot) : 0u;
+#endif
 #pragma unroll
             for (int q = 0; q < UA; q++) {
                 cu[q] = (int)(rr[q] & 0xffffu);
@@ -1162,6 +1172,7 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
     if (valid) {
         a.core[v] = k;
         a.rec[v] = pack_rec(k, cold);
+        a.e16[v] = (unsigned short)min(k, (int)RSAT);
         a.oldc[v] = cold;
         if (k > 0) a.histo[hb + k] = sum;  // cap bin := cnt
         int L = scan_len(a, hb + 1, (int)d, k);
@@ -1368,7 +1379,7 @@ static int hc_npass(long long n, uint32_t flags, int rb = 4) {
 }
 
 struct HcLayout {
-    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
+    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, e16, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
         elc, elt, total;
     long long nwords, scap, hcap, nbcap;
     size_t eltb;
@@ -1395,6 +1406,7 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags, long long
     L.c8 = b; b += align256(sizeof(shadow_t) * (size_t)n);
     L.c16 = b; b += align256(sizeof(unsigned short) * (size_t)n);
     L.rec = b; b += align256(sizeof(unsigned) * (size_t)n);
+    L.e16 = b; b += align256(sizeof(unsigned short) * (size_t)n);
     L.oldc = b; b += align256(sizeof(int) * (size_t)n);
     L.F = b; b += align256(sizeof(int) * (size_t)n);
     L.BC = b; b += align256(sizeof(int) * (size_t)n);
@@ -1475,6 +1487,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.c8 = (shadow_t *)(p + L.c8);
     a.c16 = (unsigned short *)(p + L.c16);
     a.rec = (unsigned *)(p + L.rec);
+    a.e16 = (unsigned short *)(p + L.e16);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
     a.BC = (int *)(p + L.BC);
@@ -1983,6 +1996,7 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.c8 = (shadow_t *)(p + L.c8);
     a.c16 = (unsigned short *)(p + L.c16);
     a.rec = (unsigned *)(p + L.rec);
+    a.e16 = (unsigned short *)(p + L.e16);
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
     a.BC = (int *)(p + L.BC);
