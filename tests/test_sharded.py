@@ -323,6 +323,36 @@ def test_loopback_peel_parity(parts):
 
 
 @pytest.mark.gpu
+def test_peel_shard_step_checks():
+    """pico_peel_shard_*: a frontier buffer shorter than nloc, k < 1 and a
+    negative total are PICO_EINVAL; an isolated-only shard reports INT32_MAX."""
+    import paper_2402_15253_b200 as pico
+    dev = torch.device("cuda:0")
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    rp_t, ci_t = torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev)
+    lib = pico.load()
+    n = rp.size - 1
+    sh = sharded.DevicePeelShard(rp_t, ci_t, 0, n)
+    try:
+        c, km = ctypes.c_int64(), ctypes.c_int32()
+        small = torch.empty(n - 1, dtype=torch.int32, device=dev)
+        assert lib.pico_peel_shard_scan(sh.h, 1, small.data_ptr(), n - 1, ctypes.byref(c), ctypes.byref(km)) == 1
+        assert lib.pico_peel_shard_scan(sh.h, 0, sh.front.data_ptr(), n, ctypes.byref(c), ctypes.byref(km)) == 1
+        assert lib.pico_peel_shard_apply(sh.h, None, -1, sh.front.data_ptr(), n, ctypes.byref(c),
+                                         ctypes.byref(km)) == 1
+        assert sh.kmin0 == int(np.diff(rp)[np.diff(rp) > 0].min())
+    finally:
+        sh.close()
+    iso = torch.zeros(4, dtype=torch.int64, device=dev)  # three isolated vertices
+    sh = sharded.DevicePeelShard(iso, torch.empty(0, dtype=torch.int32, device=dev), 0, 3)
+    try:
+        assert sh.kmin0 == sharded.INT32_MAX
+        assert sh.result().tolist() == [0, 0, 0]
+    finally:
+        sh.close()
+
+
+@pytest.mark.gpu
 def test_loopback_peel_c1():
     rp, ci = synth.to_numpy(*synth.CONFIGS["C1"].build())
     dev = torch.device("cuda:0")
