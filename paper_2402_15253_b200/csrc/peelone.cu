@@ -37,9 +37,6 @@
 #ifndef PICO_PO_PER
 #define PICO_PO_PER 2  // resident CTAs per SM of the persistent level kernel
 #endif
-#ifndef PICO_PO_MINB
-#define PICO_PO_MINB 1
-#endif
 
 namespace pico {
 
@@ -228,7 +225,7 @@ __global__ void po_init_kernel(PoArgs a) {
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(512, PICO_PO_MINB) po_levels_kernel(PoArgs a) {
+__global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
     constexpr bool CLAMP_SUB = MODE == 1;
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
