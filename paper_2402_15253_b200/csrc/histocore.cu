@@ -911,9 +911,10 @@ __device__ void update_phase(const HcArgs &a, int t) {
         for (int j0 = 0; j0 < total; j0 += 32 * UA) {
             ArcStep<UA> cur = nx;
             if (PICO_ARC_PF && j0 + 32 * UA < total) arc_fetch<UA>(nx, j0 + 32 * UA, total, excl, b, rows, cold);
-            // the UA record gathers are issued back to back (a fallback load
-            // between them would serialise them: ncu showed each gather waited
-            // for before the next one issued); saturated halves resolve after
+            // the UA estimate gathers (2-byte e16, or the 4-byte record) are
+            // issued back to back (a fallback load between them would
+            // serialise them: ncu showed each gather waited for before the
+            // next one issued); saturated values resolve after
             int cu[UA];
             unsigned rr[UA];
 #pragma unroll
