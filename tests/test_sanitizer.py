@@ -1,7 +1,7 @@
 """compute-sanitizer memcheck / racecheck / synccheck over every
 kernel family of libpico on small graphs (HistoCore push / pull / host loop /
-debug check, PeelOne, CntCore, NbrCore, the sharded kernels in loopback, the
-decremental update)."""
+debug check, PeelOne, CntCore, NbrCore, the sharded HistoCore and PeelOne kernels in loopback,
+the decremental update)."""
 import os
 import re
 import shutil
@@ -26,6 +26,7 @@ for algo, fl in (("histocore", 0), ("histocore", pico.F_PULL_ALWAYS | pico.F_TIN
     pico.coreness(rp, ci, algo=algo, flags=fl)
 if %r:
     sharded.coreness_loopback(rp, ci, 3, pico.F_PULL_ALWAYS)
+    sharded.coreness_loopback_peel(rp, ci, 3, pico.F_TINY_TILES)
     d = pico.DynamicCoreness(rp, ci)
     src = torch.repeat_interleave(torch.arange(rp.numel() - 1, device=rp.device), rp[1:] - rp[:-1])
     m = src < ci
