@@ -132,37 +132,61 @@ __device__ __forceinline__ int clamp_dec(int *p, int c, int k) {
 }
 
 // one sub-round of level k: process queue entries [lo, hi).  Entries hold at
-// most `seg` (<= 32) arcs, so one warp takes one entry per iteration (lanes =
-// arcs, one gather + one clamp in flight per lane): a sub-round's latency is a
-// single memory round trip per entry instead of a serial walk of long rows.
+// most `seg` (<= 32) arcs, so one warp takes PICO_PO_U entries per iteration
+// (lanes = arcs, U gathers + U clamps in flight per lane): a sub-round's
+// latency is a few memory round trips instead of a serial walk of long rows.
+#ifndef PICO_PO_U
+#define PICO_PO_U 2  // queue entries per warp iteration (independent chains in flight)
+#endif
 template <int MODE, bool STATS>
 __device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long lo, unsigned long long hi) {
+    constexpr int U = PICO_PO_U;
     const int lane = lane_id();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     int kmin = INT_MAX;
     long long nproc = 0, st_arcs = 0, st_dec = 0;
-    for (unsigned long long i = lo + gwarp; i < hi; i += nwarps) {
-        long long e = __ldcg(a.Q + i);
-        int v = (int)(e >> 32);
-        int s = (int)(e & 0xffffffffll);
-        long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-        long long b = r0 + (long long)s * a.seg;
-        int len = (int)min((long long)a.seg, r1 - b);
-        bool push = false;
-        int u = 0;
-        if (lane < len) {
-            u = __ldg(a.ci + b + lane);
-            int c = __ldcg(a.core + u);
-            if (STATS) st_arcs++;
-            if (c > k) {  // guard core[u] > k
-                int old = clamp_dec<MODE>(a.core + u, c, k);
-                if (STATS) st_dec += (old > k);
-                push = (old == k + 1);
-                if (old - 1 > k) kmin = min(kmin, old - 1);
+    // iteration it takes entries lo + (it*U + q)*nwarps + gwarp, q < U: the U
+    // entries' loads, gathers and clamps are issued together
+    for (unsigned long long i0 = lo + gwarp; i0 < hi; i0 += (unsigned long long)nwarps * U) {
+        int u[U], c[U];
+        bool in[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            unsigned long long i = i0 + (unsigned long long)q * nwarps;
+            in[q] = false;
+            u[q] = 0;
+            if (i < hi) {
+                long long e = __ldcg(a.Q + i);
+                int v = (int)(e >> 32);
+                int s = (int)(e & 0xffffffffll);
+                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+                long long b = r0 + (long long)s * a.seg;
+                int len = (int)min((long long)a.seg, r1 - b);
+                if (lane < len) {
+                    in[q] = true;
+                    u[q] = __ldg(a.ci + b + lane);
+                }
             }
         }
-        nproc += po_push(a, push, u);
+#pragma unroll
+        for (int q = 0; q < U; q++) c[q] = in[q] ? __ldcg(a.core + u[q]) : 0;
+        bool push[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            push[q] = false;
+            if (in[q]) {
+                if (STATS) st_arcs++;
+                if (c[q] > k) {  // guard core[u] > k
+                    int old = clamp_dec<MODE>(a.core + u[q], c[q], k);
+                    if (STATS) st_dec += (old > k);
+                    push[q] = (old == k + 1);
+                    if (old - 1 > k) kmin = min(kmin, old - 1);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) nproc += po_push(a, push[q], u[q]);
     }
     kmin = warp_min(kmin);
     // po_push returns the warp-wide count to every lane: lane 0 holds the total
