@@ -35,7 +35,7 @@
 #include "kernels.h"
 
 #ifndef PICO_PO_PER
-#define PICO_PO_PER 2  // resident CTAs per SM of the persistent level kernel
+#define PICO_PO_PER 3  // resident CTAs per SM of the persistent level kernel
 #endif
 
 namespace pico {
