@@ -2,22 +2,29 @@
 """bench.py -- k-core decomposition throughput on B200 (BASELINE.json metric:
 "k-core decomposition edges/sec and ms (1/2/4/8 B200), % of HBM roofline").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config T]
                     [--algo histocore|peelone] [--impl pico|reference]
 
 A step = one coreness computation of the whole graph through the C ABI
 (pico_coreness_ex: device-resident CSR in, device-resident coreness out,
 workspace allocation included).  value = undirected edges m
-/ step time (edges/s).  Inputs (colidx 4*2m bytes, histogram 4*2m bytes) are
-larger than the 126 MB L2, so no explicit flush is needed between steps.
+/ step time (edges/s).  At T the inputs (colidx 8.4 GB, histogram 8.4 GB)
+are far larger than the 126 MB L2; small configs flush L2 between steps.
 
-N = 1: the HistoCore primary kernel on configs[1] (LiveJournal-shaped); PeelOne
-is measured on the same graph and reported alongside.  N > 1 (torchrun, one
-process per GPU): sharded HistoCore over a 1-D vertex partition,
-value = m / max-over-ranks step time, "scaling": "strong".
+N = 1: the HistoCore primary kernel on the north-star "1B-edge RMAT" (config
+T: RMAT-26, edge factor 16, 2^30 samples), with PeelOne on the
+same graph alongside, parity against the serial BZ oracle in the same run,
+and the other single-GPU configs (--extras, default C2,C3) timed after it.
+roofline.frac = the METHOD's algorithmic bytes of the round kernel (SURVEY
+8(d) B_alg with S_t = sum of deg over C_t) / its CUDA-event time / the
+measured HBM peak; the implementation's own extra traffic (pull streaming,
+edge-list build, compaction) is reported apart as impl_bytes.
+N > 1 (torchrun, one process per GPU): sharded HistoCore over a 1-D vertex
+partition, value = m / max-over-ranks step time.
 
 --impl reference: the CPU oracle (serial Batagelj-Zaversnik, oracle/) timed on
-this box's host cores on the same workload -- the reference arm of this tier.
+this box's host cores -- the reference arm of this tier -- on a bounded sample
+of the workload (the same RMAT recipe at scale 22) so the run ends in minutes.
 """
 from __future__ import annotations
 
@@ -34,7 +41,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "k-core decomposition edges/sec and ms (1/2/4/8 B200), % of HBM roofline"
 UNIT = "edges/s"
-DEFAULT_CONFIG = "C2"
+DEFAULT_CONFIG = "T"
 
 
 def log(*a):
@@ -45,22 +52,35 @@ def log(*a):
 # roofline model: algorithmic bytes per kernel slot (DESIGN.md "Algorithmic
 # bytes"; SURVEY 8(d) 4-byte access model, each logical access counted once)
 # ---------------------------------------------------------------------------
-def hc_bytes(n: int, m: int, st: dict, f1: int, relabelled: bool = False) -> dict:
-    """B_alg = 8(n+1) + 4*2m [colidx] + 4*2m [gather deg] + 4*W1
-    [init slots] + 12n [core/oldcore init, initial cnt] + sum_t (32|F_t| +
-    4 bins_t + 8 S_t + 16 G_t), split by kernel slot: degree = rowptr + the
-    two estimate arrays; init = colidx + degree gathers + W1 + core + the
-    round-1 frontier (32|F_1|); rounds = the per-round terms for t >= 2 with
-    S_t = arcs scanned (push: rows of C_t; pull: rows streamed) and G_t =
-    guarded arcs (two 4 B read + 4 B write RMWs)."""
+def hc_bytes(n: int, m: int, st: dict, f1: int, s_method: int, relabelled: bool = False) -> dict:
+    """SURVEY 8(d) METHOD bytes: B_alg = 8(n+1) + 4*2m [colidx] + 4*2m [gather
+    deg] + 4*W1 [init slots] + 12n [core/oldcore init, initial cnt] + sum_t
+    (32|F_t| + 4 bins_t + 8 S_t + 16 G_t), split by kernel slot: degree =
+    rowptr + the two estimate arrays; init = colidx + degree gathers + W1 +
+    core + the round-1 frontier (32|F_1|); rounds = the per-round terms, with
+    S_t = sum_{v in C_t} deg(v) (the method's scanned arcs, ``round_arcs``)
+    and G_t = guarded arcs (two 4 B read + 4 B write RMWs).  The arcs a pull
+    round streams beyond S_t, the bucketed edge list and the compaction are
+    this implementation's own traffic: see ``hc_impl_bytes``."""
     arcs = 2 * m
     degree = 8 * (n + 1) + 8 * n
     init = 8 * arcs + 4 * st["init_slots_written"] + 4 * n + 32 * f1
-    rounds = (32 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * st["arcs_scanned"]
+    rounds = (32 * (st["frontier_total"] - f1) + 4 * st["bins_read"] + 8 * s_method
               + 16 * st["guarded_arcs"])
-    # the bucketed edge list of the pull rounds is this implementation's own
-    # overhead, not a term of the method: 0 algorithmic bytes
-    out = {"degree": degree, "init": init, "rounds": rounds, "edgelist": 0}
+    return {"degree": degree, "init": init, "rounds": rounds}
+
+
+def hc_impl_bytes(n: int, m: int, st: dict, s_method: int, relabelled: bool, npass: int) -> dict:
+    """Bytes this implementation moves that are NOT terms of the method:
+    pull rounds stream every arc of the bucketed edge list (8 B: the u and v
+    columns) instead of the rows of C_t; the edge-list build reads colidx
+    twice and writes the two columns (plus the row-owner column when
+    bucketed); the compaction remaps colidx (relabel_bytes)."""
+    arcs = 2 * m
+    pull_extra = 8 * max(st["arcs_scanned"] - s_method, 0) + 4 * st["pull_rounds"] * arcs
+    out = {"pull_stream_extra": pull_extra}
+    if st["pull_rounds"] or npass:
+        out["edgelist"] = (24 if npass > 1 else 8) * arcs
     if relabelled:
         out["relabel"] = relabel_bytes(n, m)
     return out
@@ -79,11 +99,10 @@ def i2c_bytes(n: int, m: int, st: dict, relabelled: bool = False) -> dict:
 
 
 def relabel_bytes(n: int, m: int) -> int:
-    """Internal relabel: degree keys (rowptr 8(n+1), keys+ids 8n), radix sort of
-    n (key, id) pairs (4 passes x 16 B), perm/rowptr2 (12n), row copy (rowptr
-    16 per row, colidx read + perm gather + colidx2 write = 12 per arc) and the
-    final coreness gather (12n)."""
-    return 8 * (n + 1) + 8 * n + 64 * n + 12 * n + 16 * n + 12 * 2 * m + 12 * n
+    """Internal compaction (relabel.cu): bitmap of non-isolated ids (rowptr
+    8(n+1)), rowptr2 + inverse map (12 n), the colidx remap (read + write, 8
+    B per arc; the rank words are L2-resident) and the coreness map-back (8 n)."""
+    return 8 * (n + 1) + 12 * n + 8 * 2 * m + 8 * n
 
 
 def po_bytes(n: int, m: int, st: dict, relabelled: bool = False) -> dict:
@@ -208,14 +227,36 @@ def oracle_baseline(rp_np, ci_np, budget_s: float = 12.0, max_runs: int = 5):
     return core, times
 
 
+# the reference arm's bounded sample of each workload: the same generator
+# recipe at a scale whose serial BZ takes a few seconds per step
+REF_SAMPLE = {"T": ("rmat", 22, 16 << 22, (0.57, 0.19, 0.19, 0.05), 6, 0.0, False),
+              "C4": ("kron", 22, (1_400_000_000 >> 4), (0.57, 0.19, 0.19, 0.05), 4, 0.1, True),
+              "C5": ("rmat", 22, 16 << 22, (0.57, 0.19, 0.19, 0.05), 5, 0.0, False)}
+
+
+def reference_graph(config: str, device):
+    """The graph the reference arm times: the config itself when its serial BZ
+    takes seconds, else the same recipe at scale 22 (REF_SAMPLE)."""
+    import synth
+    if config not in REF_SAMPLE:
+        cfg, rp, ci = build_graph(config, device)
+        return cfg, rp, ci, f"full {config} graph"
+    kind, scale, samples, abcd, seed, noise, compact = REF_SAMPLE[config]
+    sc = synth.GraphConfig(f"{config}-sample", kind, scale, samples, abcd=abcd, seed=seed, noise=noise,
+                           compact=compact)
+    rp, ci = sc.build(device=device)
+    return synth.CONFIGS[config], rp, ci, (f"{config} recipe at scale {scale} ({samples} samples, seed {seed}): "
+                                           "a bounded sample of the workload")
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle (serial BZ) as it stands."""
+    """--impl reference: the CPU oracle (serial BZ) as it stands, on the host."""
     import torch
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
-    cfg, rp, ci = build_graph(args.config, dev)
+    cfg, rp, ci, what = reference_graph(args.config, dev)
     import synth
     rp_np, ci_np = synth.to_numpy(rp, ci)
     del rp, ci
@@ -231,11 +272,12 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     val = m / t
-    sample = f"full {args.config} graph (n={n}, m={m}) per step, serial BZ bucket peel"
+    sample = f"{what} (n={n}, m={m}) per step, serial BZ bucket peel on 1 host core"
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": {"workload": cfg.note, "config": args.config, "n": n, "m": m, "algo": "oracle_bz"},
+           "config": {"workload": cfg.note, "config": args.config, "n": n, "m": m, "algo": "oracle_bz",
+                      "sample": what},
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "gpu_launches": 0}
@@ -243,19 +285,115 @@ def run_reference(args):
     return 0
 
 
-def time_steps(fn, steps, warmup, stream):
+L2_BYTES = 126 << 20
+
+
+def timed_steps(fn, steps: int, warmup: int, stream, flush_bytes: int = 0):
+    """Run `warmup` untimed steps, then `steps` steps each bracketed by CUDA
+    events on `stream`; between timed steps an optional L2 flush (a write of
+    `flush_bytes` > L2, outside the event pairs).  Returns the mean step ms."""
     import torch
     for _ in range(warmup):
         fn()
+    flush = torch.empty(flush_bytes // 4, dtype=torch.int32, device="cuda") if flush_bytes else None
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    evs = []
     for _ in range(steps):
+        if flush is not None:
+            flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         fn()
-    e1.record(stream)
+        e1.record(stream)
+        evs.append((e0, e1))
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / steps
+    return sum(a.elapsed_time(b) for a, b in evs) / max(steps, 1)
+
+
+def measure_algo(pico, rp, ci, algo: str, args, stream, flush_bytes: int, peak: float, with_clocks=True):
+    """One algorithm on one device-resident graph: an untimed instrumented run
+    (iteration counts, work counters, per-round arcs), a per-kernel pass
+    (library CUDA events on the launch stream, PICO_F_TIMING), then the timed
+    headline steps WITHOUT instrumentation."""
+    import numpy as np
+    import torch
+    n, m = rp.numel() - 1, ci.numel() // 2
+    st = pico.Stats()
+    fs = np.zeros(1 << 16, dtype=np.int64)
+    ra = np.zeros(1 << 16, dtype=np.int64)
+    core = pico.coreness(rp, ci, algo=algo, flags=pico.F_STATS | args.flags, stats=st,
+                         frontier_sizes=fs, round_arcs=ra)
+    torch.cuda.synchronize()
+    sd = st.to_dict()
+    # per-kernel times: a separate instrumented pass (events created per launch slot)
+    acc = {"ms": {}, "n": 0}
+
+    def kstep():
+        s2 = pico.Stats()
+        pico.coreness(rp, ci, algo=algo, flags=pico.F_TIMING | args.flags, stats=s2, out=core)
+        for k, v in s2.to_dict()["kernel_ms"].items():
+            acc["ms"][k] = acc["ms"].get(k, 0.0) + v
+        acc["n"] += 1
+
+    kstep()
+    acc = {"ms": {}, "n": 0}
+    for _ in range(max(3, min(args.steps, 5))):
+        kstep()
+    kms = {k: v / acc["n"] for k, v in acc["ms"].items()}
+    # headline steps: the plain call, no per-kernel events
+    cnt = {"launches": 0}
+
+    def step():
+        s3 = pico.Stats()
+        pico.coreness(rp, ci, algo=algo, flags=args.flags, stats=s3, out=core)
+        cnt["launches"] += s3.kernel_count
+
+    if with_clocks:
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            ms = timed_steps(step, args.steps, args.warmup, stream, flush_bytes)
+        clocks = clk.summary()
+    else:
+        ms = timed_steps(step, args.steps, args.warmup, stream, flush_bytes)
+        clocks = None
+    launches = cnt["launches"] // (args.steps + args.warmup) * args.steps
+    relabelled = "relabel" in kms
+    ran = {0: "histocore", 1: "peelone"}.get(sd.get("algo"), algo) if algo == "auto" else algo
+    l2r = sd["rounds"]
+    ra_list = [int(x) for x in ra[:l2r]] if ran == "histocore" else None
+    impl = {}
+    if ran == "histocore":
+        s_method = int(sum(ra_list)) if ra_list else 0
+        byts = hc_bytes(n, m, sd, int(fs[0]) if l2r > 0 else 0, s_method, relabelled)
+        impl = hc_impl_bytes(n, m, sd, s_method, relabelled, 1 if "edgelist" in kms else 0)
+    elif ran == "peelone":
+        byts = po_bytes(n, m, sd, False)
+        if relabelled:
+            impl = {"relabel": relabel_bytes(n, m)}
+    else:
+        byts = i2c_bytes(n, m, sd, False)
+        if relabelled:
+            impl = {"relabel": relabel_bytes(n, m)}
+    dom = max((k for k in kms if k in byts), key=kms.get)
+    ach = byts[dom] / (kms[dom] * 1e-3) / 1e9
+    total_b = sum(byts.values())
+    res = {
+        "ms": ms, "edges_per_s": m / (ms * 1e-3), "arcs_per_s": 2 * m / (ms * 1e-3),
+        "rounds_l2": sd["rounds"], "levels": sd["levels"], "subrounds": sd["subrounds"], "kmax": sd["kmax"],
+        "kernel_ms_per_step": kms, "alg_bytes": byts, "impl_bytes": impl,
+        "stats": {k: sd[k] for k in ("frontier_total", "init_slots_written", "arcs_scanned",
+                                     "guarded_arcs", "bins_read", "pushes", "alive_scanned",
+                                     "segments", "hub_fallbacks", "pull_rounds")},
+        "frontier_sizes": [int(x) for x in fs[:min(max(sd["rounds"], sd["levels"]), 4096)]],
+        "round_arcs": ra_list,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak,
+                     "whole_step_frac": total_b / (ms * 1e-3) / 1e9 / peak,
+                     "whole_step_frac_incl_impl": (total_b + sum(impl.values())) / (ms * 1e-3) / 1e9 / peak},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    return core, res
 
 
 def bench_single(args):
@@ -268,12 +406,15 @@ def bench_single(args):
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
+    peak, peak_src = hbm_peak()
     cfg, rp, ci = build_graph(args.config, dev)
     n, m = rp.numel() - 1, ci.numel() // 2
-    deg = (rp[1:] - rp[:-1])
-    dmax = int(deg.max().item())
-    del deg
-    peak, peak_src = hbm_peak()
+    dmax = int((rp[1:] - rp[:-1]).max().item()) if n else 0
+    big = 4 * 2 * m > 4 * L2_BYTES
+    flush_bytes = 0 if big else 4 * L2_BYTES
+    l2_flush = ("none: inputs larger than L2 (colidx %.0f MB + histogram %.0f MB vs 126 MB L2)"
+                % (8 * m / 1e6, 8 * m / 1e6)) if big else \
+        "L2 flushed between timed steps (504 MB buffer write outside the step events)"
 
     results = {}
     algos = [args.algo] + ([a for a in ("histocore", "peelone") if a != args.algo] if args.both else [])
@@ -284,74 +425,21 @@ def bench_single(args):
     algos = list(dict.fromkeys(algos))  # (the main algorithm first, once)
     core_ref = None
     for algo in algos:
-        # untimed instrumented run: iteration counts + work counters for B_alg
-        st = pico.Stats()
-        fs = np.zeros(1 << 16, dtype=np.int64)
-        ra = np.zeros(1 << 16, dtype=np.int64)
-        core = pico.coreness(rp, ci, algo=algo, flags=pico.F_STATS | args.flags, stats=st,
-                             frontier_sizes=fs, round_arcs=ra)
-        torch.cuda.synchronize()
-        sd = st.to_dict()
-        # timed steps (per-kernel CUDA events recorded by the library, PICO_F_TIMING)
-        acc = {"ms": {}, "launches": {}, "count": 0}
-
-        def step():
-            s2 = pico.Stats()
-            pico.coreness(rp, ci, algo=algo, flags=pico.F_TIMING | args.flags, stats=s2, out=core)
-            d = s2.to_dict()
-            for k, v in d["kernel_ms"].items():
-                acc["ms"][k] = acc["ms"].get(k, 0.0) + v
-            acc["count"] += d["kernel_count"]
-
-        for _ in range(args.warmup):
-            step()
-        acc = {"ms": {}, "launches": {}, "count": 0}
-        torch.cuda.synchronize()
-        with ClockSampler(0) as clk:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.steps):
-                step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
-        kms = {k: v / args.steps for k, v in acc["ms"].items()}
-        rl = "relabel" in kms
-        ran = {0: "histocore", 1: "peelone"}.get(sd.get("algo"), algo) if algo == "auto" else algo
-        if ran == "histocore":
-            byts = hc_bytes(n, m, sd, int(fs[0]) if sd["rounds"] > 0 else 0, rl)
-        elif ran == "peelone":
-            byts = po_bytes(n, m, sd, rl)
-        else:
-            byts = i2c_bytes(n, m, sd, rl)
-        dom = max(kms, key=kms.get)
-        ach = byts.get(dom, 0) / (kms[dom] * 1e-3) / 1e9
-        total_b = sum(byts.values())
-        results[algo] = {
-            "ms": ms, "edges_per_s": m / (ms * 1e-3), "arcs_per_s": 2 * m / (ms * 1e-3),
-            "rounds_l2": sd["rounds"], "levels": sd["levels"], "kmax": sd["kmax"],
-            "kernel_ms_per_step": kms, "alg_bytes": byts,
-            "stats": {k: sd[k] for k in ("frontier_total", "init_slots_written", "arcs_scanned",
-                                         "guarded_arcs", "bins_read", "pushes", "alive_scanned",
-                                         "segments", "hub_fallbacks", "pull_rounds")},
-            "frontier_sizes": [int(x) for x in fs[:min(max(sd["rounds"], sd["levels"]), 64)]],
-            "round_arcs": [int(x) for x in ra[:min(sd["rounds"], 64)]] if algo == "histocore" else None,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": ncu_traffic(args.config, algo, dom),
-                         "peak_source": peak_src,
-                         "whole_step_frac": total_b / (ms * 1e-3) / 1e9 / peak,
-                         # the second ceiling: L2 throughput of the same kernel, % of
-                         # peak, time-weighted over its ncu capture (profiles/ncu_traffic.json)
-                         "l2_throughput_pct": ncu_slot(args.config, algo, dom).get("l2_throughput_pct")},
-            "gpu_launches": acc["count"] // max(args.steps, 1) * args.steps,
-            "clocks": clk.summary(),
-        }
+        core, res = measure_algo(pico, rp, ci, algo, args, stream, flush_bytes, peak)
+        res["roofline"]["peak_source"] = peak_src
+        res["roofline"]["traffic"] = ncu_traffic(args.config, algo, res["roofline"]["kernel"])
+        res["roofline"]["l2_throughput_pct"] = ncu_slot(args.config, algo, res["roofline"]["kernel"]).get(
+            "l2_throughput_pct")
         if core_ref is None:
             core_ref = core.cpu().numpy()
         else:
-            results[algo]["agrees_with_" + algos[0]] = bool(np.array_equal(core.cpu().numpy(), core_ref))
-        log(f"[bench] {algo}: {ms:.3f} ms/step, {m / (ms * 1e-3) / 1e9:.3f} G edges/s, kernels {kms}")
+            res["agrees_with_" + algos[0]] = bool(np.array_equal(core.cpu().numpy(), core_ref))
+        results[algo] = res
+        log(f"[bench] {args.config} {algo}: {res['ms']:.3f} ms/step, {res['edges_per_s'] / 1e9:.3f} G edges/s, "
+            f"frac {res['roofline']['frac']:.3f} (whole step {res['roofline']['whole_step_frac']:.3f}), "
+            f"kernels {res['kernel_ms_per_step']}")
+        del core
+        torch.cuda.empty_cache()
 
     # end to end through the C ABI with pinned HOST buffers (H2D + D2H inside)
     rp_h = rp.cpu().pin_memory()
@@ -368,16 +456,48 @@ def bench_single(args):
     e2e = {"value": m / e2e_t, "unit": UNIT, "ms_per_step": 1e3 * e2e_t,
            "h2d_bytes_per_step": 8 * (n + 1) + 4 * 2 * m, "d2h_bytes_per_step": 4 * n}
 
-    # parity vs the oracle + cpu_baseline (oracle timed on this host, 1 core)
+    # parity vs the oracle + cpu_baseline (the oracle timed on this host, 1 core)
     cpu_baseline, parity = None, "skipped"
     if not args.no_oracle:
         rp_np2, ci_np2 = synth.to_numpy(rp, ci)
-        ref, times = oracle_baseline(rp_np2, ci_np2)
+        ref, times = oracle_baseline(rp_np2, ci_np2, budget_s=10.0)
         parity = "bit-exact" if np.array_equal(ref, core_ref) and np.array_equal(out_np, ref) else "MISMATCH"
         tb = sum(times) / len(times)
         cpu_baseline = {"value": m / tb, "unit": UNIT, "cores": 1, "kind": "oracle",
-                        "sample": f"full {args.config} graph (n={n}, m={m}), serial BZ, {len(times)} runs",
+                        "sample": f"full {args.config} graph (n={n}, m={m}), serial BZ, {len(times)} run(s) "
+                                  "(also the parity reference)",
                         "ms": 1e3 * tb}
+    del rp, ci, rp_h, ci_h
+    torch.cuda.empty_cache()
+
+    # the other single-GPU configs: HistoCore and PeelOne timings (parity for these
+    # sizes is covered by tests/test_fullsize.py)
+    per_config = {}
+    for c in [x for x in args.extras.split(",") if x and x != args.config]:
+        _, rpc, cic = build_graph(c, dev)
+        nc, mc = rpc.numel() - 1, cic.numel() // 2
+        fb = 0 if 4 * 2 * mc > 4 * L2_BYTES else 4 * L2_BYTES
+        entry = {"n": nc, "m": mc}
+        cref = None
+        for algo in ("histocore", "peelone"):
+            a2 = argparse.Namespace(**vars(args))
+            a2.steps, a2.warmup = max(3, min(args.steps, 10)), 3
+            core, res = measure_algo(pico, rpc, cic, algo, a2, stream, fb, peak, with_clocks=False)
+            cn = core.cpu().numpy()
+            if cref is None:
+                cref = cn
+            entry[algo] = {k: res[k] for k in ("ms", "edges_per_s", "rounds_l2", "levels", "kmax",
+                                               "kernel_ms_per_step")}
+            entry[algo]["frac"] = res["roofline"]["frac"]
+            entry[algo]["whole_step_frac"] = res["roofline"]["whole_step_frac"]
+            entry[algo]["kernel"] = res["roofline"]["kernel"]
+            if algo == "peelone":
+                entry[algo]["agrees_with_histocore"] = bool(np.array_equal(cn, cref))
+            log(f"[bench] {c} {algo}: {res['ms']:.3f} ms/step, frac {res['roofline']['frac']:.3f}")
+            del core
+        per_config[c] = entry
+        del rpc, cic
+        torch.cuda.empty_cache()
 
     main = results[args.algo]
     out = {
@@ -386,9 +506,7 @@ def bench_single(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic",
         "config": {"workload": cfg.note, "config": args.config, "algo": args.algo, "n": n, "m": m,
-                   "arcs": 2 * m, "d_max": dmax, "kmax": main["kmax"],
-                   "l2_flush": "inputs larger than L2 (colidx %.0f MB, histogram %.0f MB > 126 MB)"
-                   % (8 * m / 1e6, 8 * m / 1e6)},
+                   "arcs": 2 * m, "d_max": dmax, "kmax": main["kmax"], "l2_flush": l2_flush},
         "roofline": main["roofline"],
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
@@ -396,8 +514,10 @@ def bench_single(args):
         "clocks": main["clocks"],
         "parity": parity,
         "iterations": {"histocore_l2": results.get("histocore", {}).get("rounds_l2"),
-                       "peelone_levels": results.get("peelone", {}).get("levels")},
+                       "peelone_levels": results.get("peelone", {}).get("levels"),
+                       "peelone_subrounds": results.get("peelone", {}).get("subrounds")},
         "per_algo": results,
+        "per_config": per_config,
     }
     print(json.dumps(out), flush=True)
     return 0
@@ -416,6 +536,8 @@ def main():
     ap.add_argument("--ablations", default="auto", choices=["auto", "on", "off"],
                     help="also time CntCore / NbrCore (auto: graphs up to 320 M arcs)")
     ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
+    ap.add_argument("--extras", default="C2,C3",
+                    help="other single-GPU configs timed after the headline (comma list; '' for none)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
                     help="sharded path: NCCL inside libpico (pico_coreness_sharded) or torch.distributed")
     ap.add_argument("--sharded", action="store_true",

@@ -32,9 +32,11 @@
  *    device and a cudaStream_t (NULL = legacy default stream).  They are
  *    stream-ordered after prior work on `stream` and BLOCKING: they return
  *    when core_out is final (the round loop needs a handful of host reads).
- *  - Re-entrancy: calls on different streams/threads may run concurrently;
- *    there is no global mutable state except a thread-local last-error
- *    string.
+ *  - Re-entrancy: calls on different streams/threads may run concurrently.
+ *    Global state: a thread-local last-error string, and one library-owned
+ *    stream-ordered memory pool per device (created on first use, release
+ *    threshold "keep", never shared with the process's default pool) from
+ *    which workspace the caller does not pass is allocated and freed.
  *  - Errors: a non-zero pico_status_t is returned; nothing is thrown across
  *    the ABI.  pico_last_error() gives a thread-local message.
  *      n < 0, m < 0, NULL pointer with n > 0, unknown algo -> PICO_EINVAL
@@ -206,6 +208,22 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
 int pico_coreness_host(const int64_t *rowptr_host, const int32_t *colidx_host, int64_t n,
                        int64_t m, int algo, int32_t *core_out_host, pico_stream_t stream,
                        uint32_t flags, pico_stats_t *stats);
+
+/* Diagnostic: the clamped decrement atomicSub>=k(core, 1, k) of PeelOne
+ * ("a single atomic transaction"), run by
+ * c concurrent device threads on ONE int32 cell holding d, with the level
+ * k, in the implementation `mode` selects: 0 = atomicSub + atomicMax(k) on
+ * overshoot (the default), 1 = atomicSub + the end-of-level repair
+ * (PICO_F_CLAMP_SUB), 2 = the CAS loop (PICO_F_CLAMP_CAS).  The same device
+ * function the PeelOne kernels call.  Outputs (host pointers): the cell's
+ * final value (after the repair for mode 1), the number of calls whose
+ * returned old value was > k (those that decremented), and the number that
+ * returned k + 1 (the dynamic-frontier push).  The clamp law:
+ * final = max(k, d - c), exactly min(c, max(d - k, 0)) calls see old > k,
+ * and exactly one sees k + 1 iff k < d <= k + c.  Blocking on `stream`.
+ * c < 0, k < 0, d < 0, an unknown mode or a NULL output -> PICO_EINVAL. */
+int pico_clamp_hammer(int mode, int32_t d, int32_t k, int64_t c, int32_t *final_out,
+                      int64_t *observed_gt_k, int64_t *observed_k1, pico_stream_t stream);
 
 /* Human-readable name of a status code (static string). */
 const char *pico_status_string(int status);

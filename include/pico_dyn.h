@@ -15,9 +15,11 @@
  *    handle-owned buffer and runs HistoCore; the caller's arrays are not
  *    kept.  Internal compaction (PICO_F_RELABEL) does not apply.
  *  - src / dst are DEVICE int32 arrays of k undirected edges {src[i], dst[i]}
- *    that must be edges of the current graph, pairwise distinct; both arcs
- *    are removed.  A missing edge, a self loop or an id out of range ->
- *    PICO_EINVAL, after which the handle is unusable (destroy it).
+ *    that must be edges of the current graph; both arcs are removed.  The
+ *    batch is canonicalised on the device first ({u, v} = {v, u}; repeated
+ *    edges, in either orientation, count once).  A missing edge, a self
+ *    loop or an id out of range -> PICO_EINVAL, detected before anything is
+ *    modified: the handle keeps the previous graph and stays usable.
  *  - Calls are blocking and ordered on the stream given at creation.
  *  - Insertions are not supported (they can raise coreness, which the
  *    decreasing Index2core iteration cannot follow from the current state).

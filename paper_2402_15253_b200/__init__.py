@@ -18,7 +18,7 @@ import numpy as np
 from ._lib import (ALGOS, F_DEBUG_INVARIANTS, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
                    F_RELABEL, F_STATS, F_TIMING, F_TINY_TILES, F_VALIDATE, PicoError, Stats, check, header_functions, load)
 
-__all__ = ["coreness", "coreness_host", "workspace_bytes", "DynamicCoreness", "PicoError", "Stats", "load",
+__all__ = ["coreness", "coreness_host", "clamp_hammer", "workspace_bytes", "DynamicCoreness", "PicoError", "Stats", "load",
            "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES",
            "F_PUSH_ONLY", "F_PULL_ALWAYS", "F_RELABEL", "F_NO_RELABEL", "F_CLAMP_CAS", "F_PREFILTER"]
 
@@ -29,6 +29,14 @@ def _algo(algo) -> int:
             raise ValueError(f"unknown algo {algo!r}; expected one of {sorted(ALGOS)}")
         return ALGOS[algo]
     return int(algo)
+
+
+def _host_i64(name, a):
+    """A caller-supplied host counter array: int64, C-contiguous, writable
+    (the library writes up to a.size entries through it)."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.int64 or not a.flags["C_CONTIGUOUS"] or not a.flags["WRITEABLE"]:
+        raise TypeError(f"{name} must be a writable C-contiguous int64 numpy array")
+    return a
 
 
 def workspace_bytes(n: int, m: int, algo="histocore", flags: int = 0) -> int:
@@ -60,24 +68,36 @@ def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspa
     if arcs % 2:
         raise ValueError("colidx length must be even (2m arcs of a symmetric graph)")
     m = arcs // 2
+    if colidx.device != rowptr.device:
+        raise ValueError("rowptr and colidx must be on the same device")
     if out is None:
         out = torch.empty(max(n, 0), dtype=torch.int32, device=rowptr.device)
+    elif (not isinstance(out, torch.Tensor) or out.dtype != torch.int32 or out.device != rowptr.device
+          or not out.is_contiguous() or out.numel() < n):
+        raise ValueError(f"out must be a contiguous int32 tensor of >= {n} elements on {rowptr.device}")
     if stream is None:
         stream = torch.cuda.current_stream(rowptr.device)
     ws_ptr, ws_bytes = None, 0
     if workspace is not None:
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     st = stats
+    if frontier_sizes is None and (round_arcs is not None or round_ns is not None):
+        raise ValueError("round_arcs / round_ns need frontier_sizes (their capacity is its size)")
     if frontier_sizes is not None:
         if st is None:
             st = Stats()
+        _host_i64("frontier_sizes", frontier_sizes)
         st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         st.frontier_sizes_cap = frontier_sizes.size
         if round_arcs is not None:
-            assert round_arcs.size >= frontier_sizes.size
+            _host_i64("round_arcs", round_arcs)
+            if round_arcs.size < frontier_sizes.size:
+                raise ValueError("round_arcs must hold at least frontier_sizes.size entries")
             st.round_arcs = round_arcs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         if round_ns is not None:
-            assert round_ns.size >= 2 * frontier_sizes.size
+            _host_i64("round_ns", round_ns)
+            if round_ns.size < 2 * frontier_sizes.size:
+                raise ValueError("round_ns must hold at least 2 * frontier_sizes.size entries")
             st.round_ns = round_ns.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
     with torch.cuda.device(rowptr.device):
         rc = lib.pico_coreness_ex(rowptr.data_ptr(), colidx.data_ptr() if arcs else None, n, m, _algo(algo),
@@ -98,12 +118,29 @@ def coreness_host(rowptr: np.ndarray, colidx: np.ndarray, algo="histocore", flag
     m = ci.size // 2
     if out is None:
         out = np.empty(max(n, 0), dtype=np.int32)
+    elif (not isinstance(out, np.ndarray) or out.dtype != np.int32 or not out.flags["C_CONTIGUOUS"]
+          or not out.flags["WRITEABLE"] or out.size < n):
+        raise ValueError(f"out must be a writable C-contiguous int32 numpy array of >= {n} elements")
     sptr = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
     rc = lib.pico_coreness_host(rp.ctypes.data, ci.ctypes.data if ci.size else None, n, m, _algo(algo),
                                 out.ctypes.data if n > 0 else None, sptr, flags,
                                 ctypes.byref(stats) if stats is not None else None)
     check(rc)
     return out
+
+
+def clamp_hammer(mode: int, d: int, k: int, c: int, stream=None):
+    """``pico_clamp_hammer``: c concurrent device threads apply PeelOne's
+    clamped decrement atomicSub>=k to one cell holding d at level k,
+    in clamp implementation ``mode`` (0 default, 1 sub + repair, 2 CAS).
+    Returns (final value, calls that saw old > k, calls that saw k + 1)."""
+    lib = load()
+    fin = ctypes.c_int32()
+    gt = ctypes.c_int64()
+    k1 = ctypes.c_int64()
+    sptr = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+    check(lib.pico_clamp_hammer(mode, d, k, c, ctypes.byref(fin), ctypes.byref(gt), ctypes.byref(k1), sptr))
+    return fin.value, gt.value, k1.value
 
 
 class DynamicCoreness:
@@ -142,11 +179,16 @@ class DynamicCoreness:
 
     def delete_edges(self, src, dst, stats: Stats | None = None, frontier_sizes=None):
         import torch
-        src = src.to(device=self.dev, dtype=torch.int32).contiguous()
-        dst = dst.to(device=self.dev, dtype=torch.int32).contiguous()
+        if src.numel() != dst.numel():
+            raise ValueError(f"src and dst must have the same length ({src.numel()} != {dst.numel()})")
+        # the copies run on the handle's stream, which the library uses
+        with torch.cuda.stream(self.stream):
+            src = src.to(device=self.dev, dtype=torch.int32).contiguous()
+            dst = dst.to(device=self.dev, dtype=torch.int32).contiguous()
         st = stats
         if frontier_sizes is not None:
             st = st or Stats()
+            _host_i64("frontier_sizes", frontier_sizes)
             st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
             st.frontier_sizes_cap = frontier_sizes.size
         check(self.lib.pico_dyn_delete_edges(self.h, src.data_ptr() if src.numel() else None,

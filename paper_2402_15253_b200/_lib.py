@@ -117,6 +117,9 @@ def load(path: str | None = None):
     lib.pico_last_error.restype = ctypes.c_char_p
     lib.pico_version.argtypes = []
     lib.pico_version.restype = i32
+    lib.pico_clamp_hammer.argtypes = [i32, ctypes.c_int32, ctypes.c_int32, i64, ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
+    lib.pico_clamp_hammer.restype = i32
     lib.pico_relabel_threshold.argtypes = []
     lib.pico_relabel_threshold.restype = i64
     _setup_shard(lib)

@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary declared in include/pico.h: argument
 // checks, workspace ownership, optional CSR validation, dispatch to the
 // HistoCore / PeelOne drivers, status codes and the thread-local last error.
+#include <mutex>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -115,18 +116,34 @@ static cudaError_t dev_info(DevInfo *d) {
     if ((e = cudaGetDevice(&d->device))) return e;
     if ((e = cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->device))) return e;
     if ((e = cudaDeviceGetAttribute(&d->coop, cudaDevAttrCooperativeLaunch, d->device))) return e;
-    // Keep freed workspace in the device's stream-ordered pool (cudaMallocAsync
-    // then costs microseconds instead of an OS round trip per call).
-    static std::atomic<unsigned long long> pool_done{0};
-    if (d->device < 64 && !(pool_done.load() & (1ull << d->device))) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
-            unsigned long long thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_done.fetch_or(1ull << d->device);
-    }
     return cudaSuccess;
+}
+
+// one library-owned pool per device: freed workspace stays in it, so
+// a repeated call allocates in microseconds instead of an OS round trip
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64];
+
+cudaError_t pico::lib_malloc_async(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool[dev]) {
+            cudaMemPoolProps pp{};
+            pp.allocType = cudaMemAllocationTypePinned;
+            pp.location.type = cudaMemLocationTypeDevice;
+            pp.location.id = dev;
+            if ((e = cudaMemPoolCreate(&g_pool[dev], &pp))) { g_pool[dev] = nullptr; return e; }
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool = g_pool[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 static void reset_stats(pico_stats_t *st) {
@@ -157,7 +174,21 @@ const char *pico_status_string(int status) {
 
 const char *pico_last_error(void) { return g_last_error.c_str(); }
 
-int pico_version(void) { return 100; }
+int pico_version(void) { return 200; }
+
+int pico_clamp_hammer(int mode, int32_t d, int32_t k, int64_t c, int32_t *final_out, int64_t *observed_gt_k,
+                      int64_t *observed_k1, cudaStream_t stream) {
+    if (mode < 0 || mode > 2 || c < 0 || k < 0 || d < 0 || !final_out || !observed_gt_k || !observed_k1)
+        return fail(PICO_EINVAL, "pico_clamp_hammer: bad argument");
+    long long gt = 0, k1 = 0;
+    int fin = 0;
+    cudaError_t e = po_clamp_hammer(mode, d, k, c, &fin, &gt, &k1, stream);
+    if (e) return cuda_fail(e, "pico_clamp_hammer");
+    *final_out = fin;
+    *observed_gt_k = gt;
+    *observed_k1 = k1;
+    return PICO_OK;
+}
 
 static const long long kRelabelMinN = 16ll << 20;  // per-vertex arrays beyond L2 reach
 
@@ -241,7 +272,7 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
     void *ws = workspace;
     bool own = false;
     if (!ws) {
-        e = cudaMallocAsync(&ws, need, s);
+        e = lib_malloc_async(&ws, need, s);
         if (e) return cuda_fail(e, "workspace allocation");
         own = true;
     }
@@ -372,9 +403,9 @@ int pico_coreness_host(const int64_t *rowptr_h, const int32_t *colidx_h, int64_t
     if (n >= (1ll << 31) - 1) return fail(PICO_ENOTSUP, "n too large");
     const size_t arcs = 2 * (size_t)m;
     void *d_rp = nullptr, *d_ci = nullptr, *d_core = nullptr;
-    cudaError_t e = cudaMallocAsync(&d_rp, sizeof(int64_t) * (size_t)(n + 1), s);
-    if (!e) e = cudaMallocAsync(&d_ci, sizeof(int32_t) * std::max<size_t>(arcs, 1), s);
-    if (!e) e = cudaMallocAsync(&d_core, sizeof(int32_t) * (size_t)n, s);
+    cudaError_t e = lib_malloc_async(&d_rp, sizeof(int64_t) * (size_t)(n + 1), s);
+    if (!e) e = lib_malloc_async(&d_ci, sizeof(int32_t) * std::max<size_t>(arcs, 1), s);
+    if (!e) e = lib_malloc_async(&d_core, sizeof(int32_t) * (size_t)n, s);
     int rc = PICO_OK;
     if (e) rc = cuda_fail(e, "device buffers");
     if (rc == PICO_OK) {
@@ -677,7 +708,7 @@ static int peel_rounds(pico_comm_t comm, PeelShard *ps, long long nloc, int *fro
             if ((size_t)total > all_cap) {
                 if (all) cudaFreeAsync(all, s);
                 all_cap = (size_t)total + (size_t)total / 4;
-                if ((e = cudaMallocAsync((void **)&all, sizeof(int) * all_cap, s))) {
+                if ((e = lib_malloc_async(&all, sizeof(int) * all_cap, s))) {
                     all = nullptr;
                     return cuda_fail(e, "alloc");
                 }
@@ -794,10 +825,10 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
     auto bail_cuda = [&](cudaError_t err, const char *w) { rc = cuda_fail(err, w); };
     auto bail_nccl = [&](ncclResult_t r, const char *w) { rc = nccl_fail(r, w); };
     do {
-        if ((e = cudaMallocAsync((void **)&meta, sizeof(long long) * (3 + 3 * P), s))) { bail_cuda(e, "alloc"); break; }
-        if ((e = cudaMallocAsync((void **)&cnt, sizeof(long long) * (2 + 2 * P), s))) { bail_cuda(e, "alloc"); break; }
-        if ((e = cudaMallocAsync((void **)&deg_g, sizeof(int) * (size_t)n_global, s))) { bail_cuda(e, "alloc"); break; }
-        if ((e = cudaMallocAsync((void **)&trip, sizeof(int) * 3 * (size_t)std::max(nloc, 1ll), s))) {
+        if ((e = lib_malloc_async(&meta, sizeof(long long) * (3 + 3 * P), s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = lib_malloc_async(&cnt, sizeof(long long) * (2 + 2 * P), s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = lib_malloc_async(&deg_g, sizeof(int) * (size_t)n_global, s))) { bail_cuda(e, "alloc"); break; }
+        if ((e = lib_malloc_async(&trip, sizeof(int) * 3 * (size_t)std::max(nloc, 1ll), s))) {
             bail_cuda(e, "alloc");
             break;
         }
@@ -851,7 +882,7 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
             if ((size_t)(3 * total) > all_cap) {
                 if (all) cudaFreeAsync(all, s);
                 all_cap = (size_t)(3 * total) + (size_t)(3 * total) / 4;
-                if ((e = cudaMallocAsync((void **)&all, sizeof(int) * all_cap, s))) { all = nullptr; bail_cuda(e, "alloc"); break; }
+                if ((e = lib_malloc_async(&all, sizeof(int) * all_cap, s))) { all = nullptr; bail_cuda(e, "alloc"); break; }
             }
             if ((nr = N.GroupStart()) != ncclSuccess) { bail_nccl(nr, "group"); break; }
             for (int r = 0; r < P && nr == ncclSuccess; r++)

@@ -1982,7 +1982,7 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     if (!e) e = cudaStreamSynchronize(s);
     if (e) { delete h; return e; }
     size_t bytes = shard_workspace_bytes(nloc, ng, h->arcs, flags, &h->tscap, &h->cubbytes);
-    if ((e = cudaMallocAsync(&h->ws, bytes, s))) { delete h; return e; }
+    if ((e = lib_malloc_async(&h->ws, bytes, s))) { delete h; return e; }
     HcLayout L = hc_layout(nloc, h->arcs, flags, ng, 8);
     h->L = L;
     h->pull_ok = hc_allow_pull(ng, flags) && h->arcs > 0;
@@ -2248,33 +2248,57 @@ cudaError_t shard_destroy(Shard *h) {
 // of the new one and the Index2core iteration from it converges to the new
 // coreness (the largest fixed point below the start; readings in DESIGN.md).
 // ===========================================================================
-__global__ void dyn_delete_kernel(HcArgs a, int *ci_own, const int *src, const int *dst, long long k, int *err) {
+// Decremental batch, step 1: canonical keys (min << 32 | max) of the k
+// undirected edges; a self loop or an id out of range flags err bit 1
+__global__ void dyn_keys_kernel(const int *src, const int *dst, long long k, int n, unsigned long long *keys,
+                                int *err) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += nt) {
+        const int x = src[i], y = dst[i];
+        if (x < 0 || x >= n || y < 0 || y >= n || x == y) {
+            atomicOr(err, 1);
+            keys[i] = ~0ull;
+            continue;
+        }
+        const unsigned lo = (unsigned)min(x, y), hi = (unsigned)max(x, y);
+        keys[i] = ((unsigned long long)lo << 32) | hi;
+    }
+}
+
+// position of the arc (x, y) in x's row of the handle's CSR copy (-1: not
+// an edge of the current graph).  Warp-collective.
+__device__ __forceinline__ long long dyn_find_arc(const HcArgs &a, const int *ci_own, int x, int y) {
+    const long long r0 = a.rp[x], r1 = a.rp[x + 1];
+    for (long long e0 = r0; e0 < r1; e0 += 32) {
+        long long e = e0 + lane_id();
+        unsigned m = __ballot_sync(FULL, e < r1 && ci_own[e] == y);
+        if (m) return e0 + __ffs(m) - 1;
+    }
+    return -1;
+}
+
+// step 2 (sorted keys; a key equal to its predecessor is a duplicate of the
+// same undirected edge and is skipped, so each arc is claimed by exactly one
+// warp): APPLY = false checks that both arcs of every edge exist (err bit 2,
+// nothing written); APPLY = true tombstones the arc in the CSR copy and in
+// the pull edge list and takes the neighbour out of the histogram.
+template <bool APPLY>
+__global__ void dyn_delete_kernel(HcArgs a, int *ci_own, const unsigned long long *keys, long long k, int *err) {
     const int lane = lane_id();
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long i = gw; i < k; i += nw) {
-        const int eu = src[i], ev = dst[i];
+        const unsigned long long key = keys[i];
+        if (key == ~0ull || (i > 0 && keys[i - 1] == key)) continue;
+        const int eu = (int)(key >> 32), ev = (int)(key & 0xffffffffu);
         for (int dir = 0; dir < 2; dir++) {
             const int x = dir ? ev : eu, y = dir ? eu : ev;
-            if (x < 0 || x >= a.n || y < 0 || y >= a.n || x == y) {
-                if (lane == 0) atomicOr(err, 1);
-                continue;
-            }
-            // the arc (x, y) in the owned CSR row of x
-            const long long r0 = a.rp[x], r1 = a.rp[x + 1];
-            long long pos = -1;
-            for (long long e0 = r0; e0 < r1; e0 += 32) {
-                long long e = e0 + lane;
-                unsigned m = __ballot_sync(FULL, e < r1 && ci_own[e] == y);
-                if (m) {
-                    pos = e0 + __ffs(m) - 1;
-                    break;
-                }
-            }
+            const long long pos = dyn_find_arc(a, ci_own, x, y);
             if (pos < 0) {
                 if (lane == 0) atomicOr(err, 2);  // not an edge of the current graph
                 continue;
             }
+            if (!APPLY) continue;
             if (lane == 0) ci_own[pos] = x;  // tombstone (one bucket: pdst is ci_own)
             if (a.npass > 1) {
                 // the arc in bucket y >> pshift of the edge list (CSR order: a
@@ -2300,7 +2324,7 @@ __global__ void dyn_delete_kernel(HcArgs a, int *ci_own, const int *src, const i
             // y leaves x's histogram
             if (lane == 0) {
                 const int cx = a.core[x], cy = a.core[y];
-                const long long hb = r0 - 1;
+                const long long hb = a.rp[x] - 1;
                 if (cy >= cx) {
                     atomicSub(a.histo + hb + cx, 1);  // cnt(x) drops: a frontier candidate
                     atomicOr(a.capd + (x >> 5), 1u << (x & 31));
@@ -2335,7 +2359,7 @@ cudaError_t dyn_create(const long long *rp, const int *ci, long long n, long lon
                        cudaStream_t s, const DevInfo &dev, pico_stats_t *st, Dyn **out) {
     Dyn *h = new Dyn();
     h->n = n; h->arcs = arcs; h->flags = flags & ~(uint32_t)(PICO_F_STATS | PICO_F_HOST_LOOP); h->s = s; h->dev = dev;
-    cudaError_t e = cudaMallocAsync(&h->ws, dyn_workspace_bytes(n, arcs, h->flags), s);
+    cudaError_t e = lib_malloc_async(&h->ws, dyn_workspace_bytes(n, arcs, h->flags), s);
     if (e) { delete h; return e; }
     char *p = (char *)h->ws + align256(hc_workspace_bytes(n, arcs, h->flags));
     h->rp = (long long *)p; p += align256(sizeof(long long) * (size_t)(n + 1));
@@ -2372,11 +2396,32 @@ cudaError_t dyn_delete(Dyn *h, const int *src, const int *dst, long long k, pico
     if ((e = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return e;
     if ((e = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)a.nwords, s))) return e;
     if ((e = cudaMemsetAsync(a.capd, 0, sizeof(unsigned) * (size_t)a.nwords, s))) return e;
-    if ((e = cudaMemsetAsync(h->err, 0, sizeof(int), s))) return e;
-    if (k > 0) dyn_delete_kernel<<<sms * 8, 256, 0, s>>>(a, h->ci, src, dst, k, h->err);
     int herr = 0;
-    if ((e = cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
+    if ((e = cudaMemsetAsync(h->err, 0, sizeof(int), s))) return e;
+    if (k > 0) {
+        // canonical keys, sorted (duplicates and reversed copies adjacent),
+        // checked, then applied: a rejected batch leaves the state untouched
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys((void *)nullptr, tb, (const unsigned long long *)nullptr,
+                                       (unsigned long long *)nullptr, k);
+        const size_t kb = align256(sizeof(unsigned long long) * (size_t)k);
+        char *buf = nullptr;
+        if ((e = lib_malloc_async(&buf, 2 * kb + align256(tb), s))) return e;
+        unsigned long long *k0 = (unsigned long long *)buf, *k1 = (unsigned long long *)(buf + kb);
+        const int kbl = (int)std::min<long long>((k + 255) / 256, (long long)sms * 8);
+        dyn_keys_kernel<<<kbl, 256, 0, s>>>(src, dst, k, (int)h->n, k0, h->err);
+        e = cub::DeviceRadixSort::SortKeys(buf + 2 * kb, tb, k0, k1, k, 0, 64, s);
+        if (!e) {
+            dyn_delete_kernel<false><<<sms * 8, 256, 0, s>>>(a, h->ci, k1, k, h->err);
+            e = cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, s);
+        }
+        if (!e) e = cudaStreamSynchronize(s);
+        if (!e && !herr) dyn_delete_kernel<true><<<sms * 8, 256, 0, s>>>(a, h->ci, k1, k, h->err);
+        cudaError_t e2 = cudaFreeAsync(buf, s);
+        if (!e) e = e2;
+        if (!e) e = cudaGetLastError();
+        if (e) return e;
+    }
     if (herr) return cudaErrorInvalidValue;
     a.allow_zero = 1;
     // SumHisto of the marked vertices -> C_1, then the rounds

@@ -18,6 +18,15 @@ struct DevInfo {
     int coop;  // cooperative launch supported
 };
 
+// stream-ordered allocation from a library-owned memory pool of the current
+// device (release threshold: keep everything; the process's default pool and
+// its other users are left alone) -- capi.cu
+cudaError_t lib_malloc_async(void **p, size_t bytes, cudaStream_t s);
+template <class T>
+inline cudaError_t lib_malloc_async(T **p, size_t bytes, cudaStream_t s) {
+    return lib_malloc_async(reinterpret_cast<void **>(p), bytes, s);
+}
+
 size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags);
 cudaError_t hc_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);
@@ -30,6 +39,9 @@ cudaError_t i2c_run(const long long *rp, const int *ci, long long n, long long a
 size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags);
 cudaError_t po_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev);
+
+cudaError_t po_clamp_hammer(int mode, int d, int k, long long c, int *final_out, long long *gt, long long *k1,
+                            cudaStream_t s);
 
 // internal compaction of the vertex ids (relabel.cu)
 struct Relabel {

@@ -463,6 +463,58 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     return cudaSuccess;
 }
 
+// pico_clamp_hammer: c threads run clamp_dec<MODE> on one cell; mode 1
+// then applies the end-of-level repair (max(k, value)) as po_levels does
+template <int MODE>
+__global__ void po_hammer_kernel(int *cell, int k, long long c, unsigned long long *cnt) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    unsigned long long gt = 0, k1 = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c; i += nt) {
+        const int g = __ldcg(cell);  // the guard read core[u] > k of po_sub_phase
+        if (g <= k) continue;
+        int old = clamp_dec<MODE>(cell, g, k);
+        gt += old > k;
+        k1 += old == k + 1;
+    }
+    if (gt) atomicAdd(cnt, gt);
+    if (k1) atomicAdd(cnt + 1, k1);
+}
+
+__global__ void po_hammer_repair_kernel(int *cell, int k) {
+    if (threadIdx.x == 0 && *cell < k) *cell = k;
+}
+
+cudaError_t po_clamp_hammer(int mode, int d, int k, long long c, int *final_out, long long *gt, long long *k1,
+                            cudaStream_t s) {
+    void *buf = nullptr;
+    cudaError_t e = lib_malloc_async(&buf, 256, s);
+    if (e) return e;
+    int *cell = (int *)buf;
+    unsigned long long *cnt = (unsigned long long *)((char *)buf + 128);
+    unsigned long long h[2] = {0, 0};
+    if (!e) e = cudaMemcpyAsync(cell, &d, sizeof(int), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), s);
+    if (!e && c > 0) {
+        int blocks = (int)std::min<long long>((c + 255) / 256, 4096);
+        if (mode == 0) po_hammer_kernel<0><<<blocks, 256, 0, s>>>(cell, k, c, cnt);
+        if (mode == 1) po_hammer_kernel<1><<<blocks, 256, 0, s>>>(cell, k, c, cnt);
+        if (mode == 2) po_hammer_kernel<2><<<blocks, 256, 0, s>>>(cell, k, c, cnt);
+        e = cudaGetLastError();
+    }
+    if (!e && mode == 1 && d > k) {  // the repair covers the level's processed vertices
+        po_hammer_repair_kernel<<<1, 32, 0, s>>>(cell, k);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cudaMemcpyAsync(final_out, cell, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaFreeAsync(buf, s);
+    if (!e) e = e2;
+    if (!e) e = cudaStreamSynchronize(s);
+    *gt = (long long)h[0];
+    *k1 = (long long)h[1];
+    return e;
+}
+
 cudaError_t po_run(const long long *rp, const int *ci, long long n, long long arcs, int *core,
                    cudaStream_t s, uint32_t flags, void *ws, pico_stats_t *st, const DevInfo &dev) {
     bool stats = flags & PICO_F_STATS;

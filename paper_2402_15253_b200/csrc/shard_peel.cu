@@ -267,7 +267,7 @@ cudaError_t pshard_create(const long long *rp, const int *ci, long long nloc, lo
     h->cubbytes = ps_cub_bytes(ng, h->arcs);
     size_t bytes = a256(sizeof(PsCtl)) + a256(sizeof(int) * n1) * 3 + a256(sizeof(long long) * (ng + 1)) * 2 +
                    a256(sizeof(int) * arcs1) * 3 + a256(sizeof(int2) * h->tscap) + a256(h->cubbytes);
-    if ((e = cudaMallocAsync(&h->ws, bytes, s))) { delete h; return e; }
+    if ((e = lib_malloc_async(&h->ws, bytes, s))) { delete h; return e; }
     char *p = (char *)h->ws;
     h->ctl = (PsCtl *)p; p += a256(sizeof(PsCtl));
     h->core = (int *)p; p += a256(sizeof(int) * n1);

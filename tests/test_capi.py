@@ -209,3 +209,51 @@ def test_sharded_abi_argument_checks():
     assert lib.pico_coreness_sharded(None, None, None, 4, 2, 0, 4, 0, None, None) == 1  # NULL comm
     assert lib.pico_comm_size(None, None, None) == 1
     assert lib.pico_comm_destroy(None) == 0
+
+
+def test_clamp_hammer_argument_errors(lib):
+    """Rejected before any device work."""
+    fin, gt, k1 = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    args = (ctypes.byref(fin), ctypes.byref(gt), ctypes.byref(k1), None)
+    assert lib.pico_clamp_hammer(3, 5, 1, 4, *args) == 1
+    assert lib.pico_clamp_hammer(0, 5, 1, -1, *args) == 1
+    assert lib.pico_clamp_hammer(0, 5, -1, 4, *args) == 1
+    assert lib.pico_clamp_hammer(0, 5, 1, 4, None, ctypes.byref(gt), ctypes.byref(k1), None) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("d,k,c", [(10, 3, 4), (10, 3, 7), (10, 3, 8), (10, 3, 100_000), (1000, 2, 997),
+                                   (1 << 20, 7, 1 << 20), (5, 5, 64), (4, 6, 32), (9, 0, 1), (9, 8, 0)])
+def test_clamp_law_hammer(mode, d, k, c):
+    """SURVEY 4 T5 / S:137 / P:273: c concurrent atomicSub>=k calls on one cell
+    holding d end at max(k, d - c); exactly min(c, d - k) of them observe an old
+    value > k, and exactly one observes k + 1 (the same-level push) iff
+    k < d <= k + c -- for every clamp implementation the PeelOne kernels use."""
+    import torch
+    torch.cuda.init()
+    fin, gt, k1 = pico.clamp_hammer(mode, d, k, c)
+    assert fin == max(k, d - c) if d > k else fin == d
+    assert gt == min(c, max(d - k, 0))
+    assert k1 == (1 if k < d <= k + c else 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["R12", "C1"])
+@pytest.mark.parametrize("algo", [0, 1])
+def test_north_star_seven_argument_call(lib, cfg, algo):
+    """The literal north-star entry point pico_coreness(rowptr, colidx, n, m,
+    algo, core_out, stream) on real graphs, called through the
+    C ABI with raw device pointers: bit-exact against the BZ oracle."""
+    import torch
+    import oracle
+    import synth
+    dev = torch.device("cuda:0")
+    rp, ci = synth.CONFIGS[cfg].build(device=dev)
+    n, m = rp.numel() - 1, ci.numel() // 2
+    out = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    rc = lib.pico_coreness(rp.data_ptr(), ci.data_ptr(), n, m, algo, out.data_ptr(), ctypes.c_void_p(s.cuda_stream))
+    assert rc == 0, lib.pico_last_error()
+    ref = oracle.bz(*synth.to_numpy(rp, ci))
+    assert np.array_equal(out.cpu().numpy(), ref)

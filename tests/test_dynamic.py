@@ -62,3 +62,51 @@ def test_decremental_batches(cfg, flags):
         assert ei.value.status == 1
     finally:
         d.close()
+
+
+def test_decremental_duplicates_and_rejection():
+    """A batch holding the same undirected edge twice and reversed is applied
+    once (each arc claimed by one warp); a batch with a missing
+    edge is rejected before anything changes and the handle stays usable."""
+    import torch
+    import paper_2402_15253_b200 as pico
+    dev = torch.device("cuda:0")
+    rp, ci = synth.to_numpy(*synth.CONFIGS["R12"].build())
+    n = rp.size - 1
+    edges = _edges(rp, ci)
+    rng = np.random.default_rng(5)
+    for flags in (0, 128 | 32):
+        d = pico.DynamicCoreness(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), flags=flags)
+        try:
+            alive = np.ones(len(edges), bool)
+            idx = rng.choice(len(edges), size=300, replace=False)
+            e = edges[idx]
+            # every edge three times: as given, reversed, as given again
+            src = np.concatenate([e[:, 0], e[:, 1], e[:, 0]]).astype(np.int32)
+            dst = np.concatenate([e[:, 1], e[:, 0], e[:, 1]]).astype(np.int32)
+            perm = rng.permutation(src.size)
+            d.delete_edges(torch.from_numpy(src[perm]), torch.from_numpy(dst[perm]))
+            alive[idx] = False
+            ref = oracle.bz(*_reduced(n, edges[alive]))
+            assert np.array_equal(d.coreness().cpu().numpy(), ref)
+            # one deleted edge among live ones: rejected, nothing applied
+            live = np.flatnonzero(alive)[:50]
+            bad = np.concatenate([edges[live], edges[idx[:1]]])
+            with pytest.raises(pico.PicoError) as ei:
+                d.delete_edges(torch.from_numpy(bad[:, 0].astype(np.int32)),
+                               torch.from_numpy(bad[:, 1].astype(np.int32)))
+            assert ei.value.status == 1
+            assert np.array_equal(d.coreness().cpu().numpy(), ref)
+            # a self loop / out-of-range id / length mismatch
+            for s_, t_ in (([3], [3]), ([n], [0]), ([-1], [2])):
+                with pytest.raises(pico.PicoError):
+                    d.delete_edges(torch.tensor(s_, dtype=torch.int32), torch.tensor(t_, dtype=torch.int32))
+            with pytest.raises(ValueError):
+                d.delete_edges(torch.tensor([1, 2], dtype=torch.int32), torch.tensor([3], dtype=torch.int32))
+            # still usable: the live edges go
+            d.delete_edges(torch.from_numpy(edges[live][:, 0].astype(np.int32)),
+                           torch.from_numpy(edges[live][:, 1].astype(np.int32)))
+            alive[live] = False
+            assert np.array_equal(d.coreness().cpu().numpy(), oracle.bz(*_reduced(n, edges[alive])))
+        finally:
+            d.close()

@@ -95,3 +95,25 @@ def test_full_size_sharded_peel_loopback(parts):
     assert (run.levels, run.subrounds, run.kmax) == (st.levels, st.subrounds, st.kmax)
     del rp, ci
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("flags", [0, 32 | 128])
+def test_full_size_frontier_sequence_c2(flags):
+    """F_t = {v : h_t(v) != h_{t-1}(v)} of the synchronous Jacobi
+    iteration, so l2 and EVERY |F_t| are pinned by oracle.jacobi_rounds --
+    here on the full C2 graph in its default schedule (pull rounds over the
+    edge list, push rounds, bench launch configuration) and with pull forced
+    in every round over a many-bucket edge list (TINY_TILES | PULL_ALWAYS)."""
+    import torch
+    import paper_2402_15253_b200 as pico
+    rp, ci = _graph("C2")
+    rp_np, ci_np = synth.to_numpy(rp, ci)
+    core_j, l2, sizes = oracle.jacobi_rounds(rp_np, ci_np)
+    st = pico.Stats()
+    fs = np.zeros(1 << 12, dtype=np.int64)
+    core = pico.coreness(rp, ci, flags=flags, stats=st, frontier_sizes=fs).cpu().numpy()
+    assert np.array_equal(core, core_j)
+    assert st.rounds == l2
+    assert [int(x) for x in fs[:l2]] == [int(x) for x in sizes]
+    del rp, ci
+    torch.cuda.empty_cache()
