@@ -271,9 +271,15 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
             c->kminb[p] = INT_MAX;  // consumed at this level's head
         }
         unsigned long long lo = lstart;
-        for (;;) {
+        for (int sub = 0;; sub++) {
             unsigned long long hi = bcast_u64(&c->q_snap);
-            if (hi == lo) break;  // uniform: every CTA read the same snapshot
+            if (hi == lo) {  // uniform: every CTA read the same snapshot
+                // an empty level has no sub-round barrier: one barrier orders
+                // the leader's resets above before the next level's scan
+                // appends to alive[p] / lowers kminb[p]
+                if (sub == 0) grid_barrier(&c->bar_arrive, &c->bar_gen);
+                break;
+            }
             po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
             grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
             lo = hi;
