@@ -177,8 +177,11 @@ typedef struct {
     /* optional caller-owned HOST array of 2 * frontier_sizes_cap entries
      * receiving, for HistoCore rounds t = 1..rounds, the device time in ns
      * (%globaltimer between grid barriers) of UpdateHisto(t) at [2(t-1)] and
-     * of the SumHisto that builds F_{t+1} at [2(t-1)+1]; may be NULL.  Filled
-     * by the persistent round kernel only (not PICO_F_HOST_LOOP). */
+     * of the SumHisto that builds F_{t+1} at [2(t-1)+1]; for PeelOne, per
+     * scanned level L = 0, 1, ... the level scan at [2L] and the drain of its
+     * dynamic frontier at [2L+1] (low 40 bits; above them the level's k at
+     * [2L] and its BSP sub-rounds at [2L+1]); may be NULL.  Filled by the persistent
+     * kernels only (not PICO_F_HOST_LOOP). */
     int64_t *round_ns;
     /* the algorithm that ran (PICO_ALGO_AUTO resolved) */
     int64_t algo;

@@ -137,6 +137,34 @@ __device__ __forceinline__ void red_or(unsigned *p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// warp-aggregated reservation of nseg segments per lane; writes (v, s) entries
+__device__ __forceinline__ void warp_append_segments(int v, int nseg, int2 *S,
+                                                     unsigned long long *nS) {
+    int incl = warp_incl_scan(nseg);
+    int total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(nS, (unsigned long long)total);
+    base = __shfl_sync(FULL, base, 0);
+    // the warp writes the `total` entries jointly (a hub's thousands of
+    // segments do not serialise on its lane): entry j belongs to the lane with
+    // the largest exclusive offset <= j
+    const int excl = incl - nseg;
+    for (int j0 = 0; j0 < total; j0 += 32) {
+        int j = j0 + lane_id();
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            int cand = lo + step;
+            int ex = __shfl_sync(FULL, excl, cand & 31);
+            if (cand < 32 && ex <= j) lo = cand;
+        }
+        int vo = __shfl_sync(FULL, v, lo);
+        int eo = __shfl_sync(FULL, excl, lo);
+        if (j < total) S[base + j] = make_int2(vo, j - eo);
+    }
+}
+
 // Block-uniform read of a control word other CTAs wrote before a barrier:
 // thread 0 loads it and broadcasts through shared memory, so a 300K-thread
 // grid issues one L2 request per CTA instead of one per thread to a single
@@ -222,6 +250,8 @@ struct Ctrl {
     alignas(128) unsigned long long q_pending;  // pushed, not fully processed
     alignas(128) unsigned long long q_snap;     // tail snapshot at the last barrier
     unsigned long long nAlive[2];  // alive list lengths (ping-pong by level)
+    unsigned long long nFar[2];    // far list lengths (ping-pong by rebuild)
+    int fmin[2];                   // min estimate in the far list (ping-pong)
     unsigned long long nProc[2];   // vertices processed per level (parity)
     unsigned long long levels;     // non-empty levels
     unsigned long long scans;      // levels scanned

@@ -191,34 +191,6 @@ __device__ __forceinline__ void set_c8(const HcArgs &a, int v, int k) {
     a.c16[v] = (unsigned short)min(k, 65535);
 }
 
-// warp-aggregated reservation of nseg segments per lane; writes (v, s) entries
-__device__ __forceinline__ void warp_append_segments(int v, int nseg, int2 *S,
-                                                     unsigned long long *nS) {
-    int incl = warp_incl_scan(nseg);
-    int total = __shfl_sync(FULL, incl, 31);
-    if (total == 0) return;
-    unsigned long long base = 0;
-    if (lane_id() == 0) base = atomicAdd(nS, (unsigned long long)total);
-    base = __shfl_sync(FULL, base, 0);
-    // the warp writes the `total` entries jointly (a hub's thousands of
-    // segments do not serialise on its lane): entry j belongs to the lane with
-    // the largest exclusive offset <= j
-    const int excl = incl - nseg;
-    for (int j0 = 0; j0 < total; j0 += 32) {
-        int j = j0 + lane_id();
-        int lo = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            int cand = lo + step;
-            int ex = __shfl_sync(FULL, excl, cand & 31);
-            if (cand < 32 && ex <= j) lo = cand;
-        }
-        int vo = __shfl_sync(FULL, v, lo);
-        int eo = __shfl_sync(FULL, excl, lo);
-        if (j < total) S[base + j] = make_int2(vo, j - eo);
-    }
-}
-
 __device__ __forceinline__ void stat_add(unsigned long long *ctr, long long x) {
     long long s = warp_sum64(x);
     if (lane_id() == 0 && s) atomicAdd(ctr, (unsigned long long)s);

@@ -88,14 +88,7 @@ __global__ void i2c_segments_kernel(I2cArgs a, const int *list, const unsigned l
             ns = (d + kSeg - 1) / kSeg;
             arcs += d;
         }
-        int incl = warp_incl_scan(ns);
-        int total = __shfl_sync(FULL, incl, 31);
-        if (total) {
-            unsigned long long base = 0;
-            if (lane_id() == 0) base = atomicAdd(&a.c[4], (unsigned long long)total);
-            base = __shfl_sync(FULL, base, 0);
-            for (int s = 0; s < ns; s++) a.SG[base + incl - ns + s] = make_int2(v, s);
-        }
+        warp_append_segments(v, ns, a.SG, &a.c[4]);  // a hub's segments written by the whole warp
     }
     long long s = warp_sum64(arcs);
     if (lane_id() == 0 && s) atomicAdd(&a.c[5], (unsigned long long)s);

@@ -34,6 +34,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef PICO_PO_KHI0
+#define PICO_PO_KHI0 32  // initial near window: vertices of degree <= 32
+#endif
 #ifndef PICO_PO_PER
 #define PICO_PO_PER 3  // resident CTAs per SM of the persistent level kernel
 #endif
@@ -47,9 +50,13 @@ struct PoArgs {
     int *core;
     int *alive0;
     int *alive1;
+    int *far0;     // near / far split of the alive vertices: alive[] ("near")
+    int *far1;     // holds those with estimate <= khi, far[] the others
+    int khi0;      // initial window bound (INT_MAX: no far list)
     long long *Q;  // (v << 32) | segment
     unsigned long long *fsz;
     unsigned long long fsz_cap;
+    unsigned long long *rtime;  // [2 fsz_cap] per scanned level: scan ns | k << 40, drain ns | sub-rounds << 40
     Ctrl *ctl;
     int seg;
 };
@@ -68,8 +75,24 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&a.ctl->q_tail, (unsigned long long)total);
     base = __shfl_sync(FULL, base, 0);
-    unsigned long long off = base + (unsigned long long)(incl - ns);
-    for (int s = 0; s < ns; s++) a.Q[off + s] = ((long long)v << 32) | s;
+    // the warp writes the `total` entries jointly, so a hub's thousands of
+    // entries do not serialise on its lane (one lane writing the 31K entries
+    // of a 1M-degree hub cost up to ~6 ms per level at RMAT-26): entry j
+    // belongs to the lane with the largest exclusive offset <= j
+    const int excl = incl - ns;
+    for (int j0 = 0; j0 < total; j0 += 32) {
+        const int j = j0 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            int cand = lo + step;
+            int ex = __shfl_sync(FULL, excl, cand & 31);
+            if (cand < 32 && ex <= j) lo = cand;
+        }
+        const int vo = __shfl_sync(FULL, v, lo);
+        const int eo = __shfl_sync(FULL, excl, lo);
+        if (j < total) a.Q[base + j] = ((long long)vo << 32) | (unsigned)(j - eo);
+    }
     return __popc(__ballot_sync(FULL, pred));
 }
 
@@ -105,6 +128,48 @@ __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, 
     }
 }
 
+// Near / far alive lists.  A level's scan walks only the near list (the alive
+// vertices with estimate <= khi): at RMAT-26 the plain scan re-read ~1.9 M alive
+// vertices at each of ~400 levels (759 M entries, a third of PeelOne's time),
+// most of them hubs far above the level.  The far list holds the others; a far
+// vertex whose estimate is decremented to khi is appended to the near list at
+// that moment (cross, po_sub_phase).  When the next level exceeds khi the far
+// list is rebuilt: khi doubles, far vertices now within it join the near list,
+// those that already crossed (estimate <= the old khi) are dropped.  The
+// level bound is min(near bound, far minimum).  The scanned set is exactly
+// what a full scan would find with estimate == k (nothing else changes).
+__device__ void po_rebuild_phase(const PoArgs &a, int khi_old, int khi, int fp, int p, long long gthread,
+                                 long long nthreads, bool stats) {
+    const long long nf = (long long)bcast_u64(&a.ctl->nFar[fp]);
+    const int *far = fp ? a.far1 : a.far0;
+    int *keepto = fp ? a.far0 : a.far1;
+    int *near = p ? a.alive1 : a.alive0;
+    int fmin = INT_MAX, kmin = INT_MAX;
+    const long long iters = (nf + nthreads - 1) / nthreads;
+    for (long long it = 0; it < iters; it++) {
+        long long i = it * nthreads + gthread;
+        bool valid = i < nf;
+        int v = 0, c = 0;
+        if (valid) {
+            v = __ldcg(far + i);
+            c = __ldcg(a.core + v);
+        }
+        const bool join = valid && c > khi_old && c <= khi;
+        const bool stay = valid && c > khi;
+        if (join) kmin = min(kmin, c);
+        if (stay) fmin = min(fmin, c);
+        warp_append(join, v, near, &a.ctl->nAlive[p]);
+        warp_append(stay, v, keepto, &a.ctl->nFar[fp ^ 1]);
+    }
+    fmin = warp_min(fmin);
+    kmin = warp_min(kmin);
+    if (lane_id() == 0) {
+        if (fmin != INT_MAX) atomicMin(&a.ctl->fmin[fp ^ 1], fmin);
+        if (kmin != INT_MAX) atomicMin(&a.ctl->kminb[p], kmin);
+        if (stats && gthread == 0) atomicAdd(&a.ctl->st_alive, (unsigned long long)nf);
+    }
+}
+
 // clamped decrement atomicSub>=k(core[u], 1, k) of P:273; returns the old
 // value (> k: the caller decremented; == k+1: it set the value to k).
 //   MODE 0 (default): atomicSub, and only if that overshot below k an
@@ -131,68 +196,105 @@ __device__ __forceinline__ int clamp_dec(int *p, int c, int k) {
     return old;
 }
 
-// one sub-round of level k: process queue entries [lo, hi).  Entries hold at
-// most `seg` (<= 32) arcs, so one warp takes PICO_PO_U entries per iteration
-// (lanes = arcs, U gathers + U clamps in flight per lane): a sub-round's
-// latency is a few memory round trips instead of a serial walk of long rows.
+// one sub-round of level k: process queue entries [lo, hi).  An entry holds
+// at most `seg` = 32 * PICO_PO_A arcs; one warp takes PICO_PO_U entries per
+// iteration and each lane A arcs of each (lane + 32 j), so U * A colidx loads,
+// core gathers and clamps are in flight per lane: a sub-round's latency is a
+// few memory round trips, and the heavy levels (at RMAT-26 four levels peel
+// 70% of the arcs through hub rows) stream U * A * 32 arcs per warp chain.
 #ifndef PICO_PO_U
 #define PICO_PO_U 2  // queue entries per warp iteration (independent chains in flight)
 #endif
+#ifndef PICO_PO_A
+#define PICO_PO_A 1  // arcs per lane per entry (entry = 32 * A arcs)
+#endif
 template <int MODE, bool STATS>
-__device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long lo, unsigned long long hi) {
-    constexpr int U = PICO_PO_U;
+__device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long lo, unsigned long long hi,
+                             int khi = INT_MAX, int *fminp = nullptr) {
+    constexpr int U = PICO_PO_U, A = PICO_PO_A, W = U * A;
     const int lane = lane_id();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    int kmin = INT_MAX;
+    int kmin = INT_MAX, fmin = INT_MAX;
     long long nproc = 0, st_arcs = 0, st_dec = 0;
+    __shared__ int s_b[2];  // CTA minima of the next-level and far bounds
+    if (threadIdx.x == 0) s_b[0] = s_b[1] = INT_MAX;
+    __syncthreads();
     // iteration it takes entries lo + (it*U + q)*nwarps + gwarp, q < U: the U
     // entries' loads, gathers and clamps are issued together
     for (unsigned long long i0 = lo + gwarp; i0 < hi; i0 += (unsigned long long)nwarps * U) {
-        int u[U], c[U];
-        bool in[U];
+        int u[W], c[W];
 #pragma unroll
         for (int q = 0; q < U; q++) {
             unsigned long long i = i0 + (unsigned long long)q * nwarps;
-            in[q] = false;
-            u[q] = 0;
+            long long b = 0;
+            int len = 0;
             if (i < hi) {
                 long long e = __ldcg(a.Q + i);
                 int v = (int)(e >> 32);
                 int s = (int)(e & 0xffffffffll);
                 long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-                long long b = r0 + (long long)s * a.seg;
-                int len = (int)min((long long)a.seg, r1 - b);
-                if (lane < len) {
-                    in[q] = true;
-                    u[q] = __ldg(a.ci + b + lane);
-                }
+                b = r0 + (long long)s * a.seg;
+                len = (int)min((long long)a.seg, r1 - b);
             }
+#pragma unroll
+            for (int j = 0; j < A; j++) u[q * A + j] = (j * 32 + lane < len) ? __ldg(a.ci + b + j * 32 + lane) : -1;
         }
 #pragma unroll
-        for (int q = 0; q < U; q++) c[q] = in[q] ? __ldcg(a.core + u[q]) : 0;
-        bool push[U];
+        for (int w = 0; w < W; w++) c[w] = u[w] >= 0 ? __ldcg(a.core + u[w]) : 0;
+        bool push[W];
+        int old[W];
+        // the W clamped decrements are issued back to back: for MODE 0 / 1 the
+        // atomicSubs first, then MODE 0's atomicMax repairs of those that
+        // overshot (independent atomics on distinct cells; issuing each
+        // clamp_dec whole serialised a round trip per arc)
 #pragma unroll
-        for (int q = 0; q < U; q++) {
-            push[q] = false;
-            if (in[q]) {
-                if (STATS) st_arcs++;
-                if (c[q] > k) {  // guard core[u] > k
-                    int old = clamp_dec<MODE>(a.core + u[q], c[q], k);
-                    if (STATS) st_dec += (old > k);
-                    push[q] = (old == k + 1);
-                    if (old - 1 > k) kmin = min(kmin, old - 1);
-                }
-            }
+        for (int w = 0; w < W; w++) {
+            const bool g = u[w] >= 0 && c[w] > k;  // guard core[u] > k
+            if (MODE == 2) old[w] = g ? clamp_dec<2>(a.core + u[w], c[w], k) : k;
+            else old[w] = g ? atomicSub(a.core + u[w], 1) : k;
+        }
+        if (MODE == 0) {
+#pragma unroll
+            for (int w = 0; w < W; w++)
+                if (u[w] >= 0 && c[w] > k && old[w] <= k) atomicMax(a.core + u[w], k);
+        }
+        bool cross[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+            if (STATS) st_arcs += u[w] >= 0;
+            if (STATS) st_dec += (old[w] > k);
+            push[w] = (old[w] == k + 1);
+            if (old[w] - 1 > k) kmin = min(kmin, old[w] - 1);
+            // a far vertex that stays far keeps the far minimum a lower bound
+            // (the next level bound min(kminb, fmin) must cover it at every
+            // later level, not only the next one)
+            if (old[w] - 1 > khi) fmin = min(fmin, old[w] - 1);
+            // a far vertex whose estimate reaches khi enters the near list
+            // (values step down by one, so exactly one decrement sees it)
+            cross[w] = old[w] - 1 == khi && khi > k;
         }
 #pragma unroll
-        for (int q = 0; q < U; q++) nproc += po_push(a, push[q], u[q]);
+        for (int w = 0; w < W; w++)
+            if (__any_sync(FULL, cross[w])) warp_append(cross[w], u[w], p ? a.alive0 : a.alive1, &a.ctl->nAlive[p ^ 1]);
+#pragma unroll
+        for (int w = 0; w < W; w++)
+            if (__any_sync(FULL, push[w])) nproc += po_push(a, push[w], u[w]);
     }
     kmin = warp_min(kmin);
-    // po_push returns the warp-wide count to every lane: lane 0 holds the total
+    fmin = warp_min(fmin);
+    // the two level bounds are reduced per CTA first (one global atomic per
+    // CTA instead of one per warp on two hot words); po_push returns the
+    // warp-wide count to every lane: lane 0 holds the total
     if (lane == 0) {
-        if (kmin != INT_MAX) atomicMin(&a.ctl->kminb[p ^ 1], kmin);
+        if (kmin != INT_MAX) atomicMin(&s_b[0], kmin);
+        if (fmin != INT_MAX) atomicMin(&s_b[1], fmin);
         if (nproc) atomicAdd(&a.ctl->nProc[p], (unsigned long long)nproc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_b[0] != INT_MAX) atomicMin(&a.ctl->kminb[p ^ 1], s_b[0]);
+        if (s_b[1] != INT_MAX && fminp) atomicMin(fminp, s_b[1]);
     }
     if (STATS) {
         long long s1 = warp_sum64(st_arcs), s2 = warp_sum64(st_dec);
@@ -231,25 +333,29 @@ __global__ void po_init_kernel(PoArgs a) {
     long long nthreads = (long long)gridDim.x * blockDim.x;
     long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long iters = (a.n + nthreads - 1) / nthreads;
-    int kmin = INT_MAX;
+    int kmin = INT_MAX, fmin = INT_MAX;
     for (long long it = 0; it < iters; it++) {
         long long v = it * nthreads + gthread;
         bool valid = v < a.n;
         int d = valid ? (int)(a.rp[v + 1] - a.rp[v]) : 0;
         if (valid) a.core[v] = d;
-        bool alive = d > 0;
-        if (alive) kmin = min(kmin, d);
-        warp_append(alive, (int)v, a.alive0, &a.ctl->nAlive[0]);
+        bool near = d > 0 && d <= a.khi0, far = d > a.khi0;
+        if (near) kmin = min(kmin, d);
+        if (far) fmin = min(fmin, d);
+        warp_append(near, (int)v, a.alive0, &a.ctl->nAlive[0]);
+        warp_append(far, (int)v, a.far0, &a.ctl->nFar[0]);
     }
     kmin = warp_min(kmin);
+    fmin = warp_min(fmin);
     if (lane_id() == 0 && kmin != INT_MAX) atomicMin(&a.ctl->kminb[0], kmin);
+    if (lane_id() == 0 && fmin != INT_MAX) atomicMin(&a.ctl->fmin[0], fmin);
 }
 
 // ---------------------------------------------------------------------------
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
+__global__ void __launch_bounds__(512, PICO_PO_PER) po_levels_kernel(PoArgs a) {
     constexpr bool CLAMP_SUB = MODE == 1;
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
@@ -257,15 +363,35 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
     Ctrl *c = a.ctl;
     int k = 0, kprev = 0;
     unsigned long long S = 0;  // global sub-round counter (claim counter parity)
+    int khi = a.khi0, fp = 0;  // near window bound, far list parity (uniform)
     for (int L = 0;; L++) {
         const int p = L & 1;
         long long na = (long long)bcast_u64(&c->nAlive[p]);
+        const long long nf = (long long)bcast_u64(&c->nFar[fp]);
         if (leader && L > 0) po_close_level(a, p ^ 1, kprev);
-        if (na == 0) break;
-        k = max(k + 1, bcast_i32(&c->kminb[p]));
+        if (na == 0 && nf == 0) break;
+        k = max(k + 1, min(bcast_i32(&c->kminb[p]), nf ? bcast_i32(&c->fmin[fp]) : INT_MAX));
+        unsigned long long ts0 = leader ? globaltimer() : 0, ts1 = 0, S0 = S;
+        if (nf && (k > khi || na == 0)) {
+            // uniform: the window is exhausted (or the near list empty): rebuild
+            // the far list with a doubled window
+            const int khi_new = (int)max((long long)khi, min(2ll * k + 16, (long long)INT_MAX - 1));
+            po_rebuild_phase(a, khi, khi_new, fp, p, gthread, nthreads, STATS);
+            grid_barrier(&c->bar_arrive, &c->bar_gen);
+            if (leader) {
+                c->nFar[fp] = 0;  // consumed; refilled at the next rebuild
+                c->fmin[fp] = INT_MAX;
+            }
+            khi = khi_new;
+            fp ^= 1;
+            // the joiners lowered kminb[p]; the far minimum is the rebuilt one
+            const long long nf2 = (long long)bcast_u64(&c->nFar[fp]);
+            k = max(k, min(bcast_i32(&c->kminb[p]), nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
+        }
         unsigned long long lstart = bcast_u64(&c->q_snap);
         po_scan_phase<STATS>(a, k, p, gthread, nthreads);
         grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
+        if (leader) ts1 = globaltimer();
         if (leader) {
             c->nAlive[p] = 0;       // alive[p] consumed; refilled at level L+1
             c->kminb[p] = INT_MAX;  // consumed at this level's head
@@ -280,7 +406,7 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
                 if (sub == 0) grid_barrier(&c->bar_arrive, &c->bar_gen);
                 break;
             }
-            po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
+            po_sub_phase<MODE, STATS>(a, k, p, lo, hi, khi, &c->fmin[fp]);
             grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
             lo = hi;
             S++;
@@ -289,7 +415,13 @@ __global__ void __launch_bounds__(512) po_levels_kernel(PoArgs a) {
             po_repair_phase(a, k, lstart, lo, gthread, nthreads);
             grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
         }
-        if (leader) c->rounds = S;  // BSP sub-rounds so far
+        if (leader) {
+            c->rounds = S;  // BSP sub-rounds so far
+            if ((unsigned long long)L < a.fsz_cap) {  // per scanned level: scan ns, drain ns | sub-rounds << 40
+                a.rtime[2 * L] = (ts1 - ts0) | ((unsigned long long)k << 40);
+                a.rtime[2 * L + 1] = (globaltimer() - ts1) | ((S - S0) << 40);
+            }
+        }
         kprev = k;
     }
 }
@@ -324,13 +456,14 @@ __global__ void po_close_kernel(PoArgs a, int p, int k) { po_close_level(a, p, k
 // host driver
 // ---------------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-static int po_seg(uint32_t flags) { return (flags & PICO_F_TINY_TILES) ? 4 : 32; }
+static int po_seg(uint32_t flags) { return (flags & PICO_F_TINY_TILES) ? 4 : 32 * PICO_PO_A; }
 
 size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags) {
     size_t b = 0;
     b += align256(sizeof(Ctrl));
     b += align256(sizeof(unsigned long long) * kFszCap);
-    b += align256(sizeof(int) * (size_t)n) * 2;
+    b += align256(sizeof(unsigned long long) * 2 * kFszCap);
+    b += align256(sizeof(int) * (size_t)n) * 4;
     b += align256(sizeof(long long) * (size_t)(n + arcs / po_seg(flags) + 64));
     return b;
 }
@@ -345,9 +478,14 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     a.ctl = (Ctrl *)p; p += align256(sizeof(Ctrl));
     a.fsz = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * kFszCap);
     a.fsz_cap = kFszCap;
+    a.rtime = (unsigned long long *)p; p += align256(sizeof(unsigned long long) * 2 * kFszCap);
     a.alive0 = (int *)p; p += align256(sizeof(int) * (size_t)n);
     a.alive1 = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.far0 = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.far1 = (int *)p; p += align256(sizeof(int) * (size_t)n);
     a.Q = (long long *)p;
+    // the host loop keeps one alive list (no far list)
+    a.khi0 = (flags & PICO_F_HOST_LOOP) ? INT_MAX : PICO_PO_KHI0;
     a.seg = po_seg(flags);
     a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core;
 
@@ -355,6 +493,8 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     Ctrl h{};
     h.kminb[0] = INT_MAX;
     h.kminb[1] = INT_MAX;
+    h.fmin[0] = INT_MAX;
+    h.fmin[1] = INT_MAX;
     if ((err = cudaMemcpyAsync(a.ctl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
 
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -449,6 +589,16 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         if (st->frontier_sizes)
             for (unsigned long long i = 0; i < hc.levels && (int64_t)i < st->frontier_sizes_cap && i < kFszCap; i++)
                 st->frontier_sizes[i] = (int64_t)lv[i];
+        if (st->round_ns && !(flags & PICO_F_HOST_LOOP)) {
+            size_t nl = (size_t)std::min<unsigned long long>(hc.scans, std::min<unsigned long long>(
+                                                                kFszCap, (unsigned long long)st->frontier_sizes_cap));
+            std::vector<unsigned long long> rt(2 * nl + 1);
+            if ((err = cudaMemcpyAsync(rt.data(), a.rtime, sizeof(unsigned long long) * 2 * nl,
+                                       cudaMemcpyDeviceToHost, s)))
+                return err;
+            if ((err = cudaStreamSynchronize(s))) return err;
+            for (size_t i = 0; i < 2 * nl; i++) st->round_ns[i] = (int64_t)rt[i];
+        }
         if (STATS) {
             st->arcs_scanned = (int64_t)hc.st_arcs;
             st->guarded_arcs = (int64_t)hc.st_guarded;
