@@ -53,6 +53,7 @@ struct PoArgs {
     int *far0;     // near / far split of the alive vertices: alive[] ("near")
     int *far1;     // holds those with estimate <= khi, far[] the others
     int khi0;      // initial window bound (INT_MAX: no far list)
+    unsigned *done;  // [n/32] processed bitmap: v entered a frontier (its coreness is final)
     long long *Q;  // (v << 32) | segment
     unsigned long long *fsz;
     unsigned long long fsz_cap;
@@ -69,6 +70,15 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     const int lane = lane_id();
     int ns = 0;
     if (pred) ns = po_nseg(__ldg(a.rp + v + 1) - __ldg(a.rp + v), a.seg);
+    if (__any_sync(FULL, pred)) {
+        // processed: later guards skip v.  Lanes whose vertices share a bitmap
+        // word (the scan's frontier comes from id-ordered blocks) OR their bits
+        // together first: one RED per word instead of up to 32 on one address
+        const int wd = pred ? (v >> 5) : -1;
+        const unsigned peers = __match_any_sync(FULL, wd);
+        const unsigned bits = __reduce_or_sync(peers, pred ? 1u << (v & 31) : 0u);
+        if (pred && lane == __ffs(peers) - 1) red_or(a.done + wd, bits);
+    }
     int incl = warp_incl_scan(ns);
     int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return 0;
@@ -240,8 +250,20 @@ __device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long l
 #pragma unroll
             for (int j = 0; j < A; j++) u[q * A + j] = (j * 32 + lane < len) ? __ldg(a.ci + b + j * 32 + lane) : -1;
         }
+        // guard core[u] > k.  Every vertex with core <= k is processed
+        // (it entered a frontier, which marks the n/8-byte `done` bitmap) except
+        // members of this level's frontier not yet marked, so "not done" is
+        // the guard up to those, for which the clamp returns old <= k and
+        // changes nothing.  The bitmap stays in L2: no DRAM sector of core[]
+        // per arc.  The CAS clamp still reads core[u] for its first compare.
+        unsigned dw[W];
 #pragma unroll
-        for (int w = 0; w < W; w++) c[w] = u[w] >= 0 ? __ldcg(a.core + u[w]) : 0;
+        for (int w = 0; w < W; w++) dw[w] = u[w] >= 0 ? __ldcg(a.done + (u[w] >> 5)) : ~0u;
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+            const bool live = !((dw[w] >> (u[w] & 31)) & 1u);
+            c[w] = live ? (MODE == 2 ? __ldcg(a.core + u[w]) : INT_MAX) : 0;
+        }
         bool push[W];
         int old[W];
         // the W clamped decrements are issued back to back: for MODE 0 / 1 the
@@ -464,6 +486,7 @@ size_t po_workspace_bytes(long long n, long long arcs, uint32_t flags) {
     b += align256(sizeof(unsigned long long) * kFszCap);
     b += align256(sizeof(unsigned long long) * 2 * kFszCap);
     b += align256(sizeof(int) * (size_t)n) * 4;
+    b += align256(sizeof(unsigned) * (size_t)((n + 31) / 32 + 1));
     b += align256(sizeof(long long) * (size_t)(n + arcs / po_seg(flags) + 64));
     return b;
 }
@@ -483,6 +506,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     a.alive1 = (int *)p; p += align256(sizeof(int) * (size_t)n);
     a.far0 = (int *)p; p += align256(sizeof(int) * (size_t)n);
     a.far1 = (int *)p; p += align256(sizeof(int) * (size_t)n);
+    a.done = (unsigned *)p; p += align256(sizeof(unsigned) * (size_t)((n + 31) / 32 + 1));
     a.Q = (long long *)p;
     // the host loop keeps one alive list (no far list)
     a.khi0 = (flags & PICO_F_HOST_LOOP) ? INT_MAX : PICO_PO_KHI0;
@@ -496,6 +520,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     h.fmin[0] = INT_MAX;
     h.fmin[1] = INT_MAX;
     if ((err = cudaMemcpyAsync(a.ctl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
+    if ((err = cudaMemsetAsync(a.done, 0, sizeof(unsigned) * (size_t)((n + 31) / 32 + 1), s))) return err;
 
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     auto tstart = [&](int slot) {
