@@ -102,6 +102,11 @@ enum {
                               /* those at or above it) and that  */
                               /* the estimates are an h-index fixed point   */
                               /* (P:138-146); a violation -> PICO_EGRAPH    */
+    PICO_F_L2_PERSIST = 16384u,/* HistoCore A/B: the push rounds' estimate   */
+                              /* gathers (n x 2 B) as a persisting L2       */
+                              /* access-policy window during the round      */
+                              /* kernel (sets and then resets the device's  */
+                              /* persisting-L2 limit: process-wide state)   */
     PICO_F_PREFILTER = 2048u, /* HistoCore: degree-bucket row order + scan   */
                               /* prefix (cuts scanned arcs ~44%; measured    */
                               /* slower on B200, so opt-in)                  */

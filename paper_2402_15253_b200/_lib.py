@@ -25,6 +25,7 @@ F_NO_RELABEL = 512
 F_CLAMP_CAS = 1024
 F_PREFILTER = 2048
 F_DEBUG_INVARIANTS = 4096
+F_L2_PERSIST = 16384
 
 K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel", "edgelist"]
 

@@ -983,6 +983,9 @@ __global__ void __launch_bounds__(256) hc_check_kernel(HcArgs a, int *bad) {
 #ifndef PICO_PULL_U
 #define PICO_PULL_U 4
 #endif
+#ifndef PICO_PULL_VEC
+#define PICO_PULL_VEC 0  // int4 loads of the edge-list columns (A/B: DESIGN.md)
+#endif
 // v-side estimate records: one GPU gathers the 4-byte records of its own
 // vertices (16|16 bits, saturated values fall back to the full arrays);
 // a shard gathers 8-byte records (32|32 bits, never saturated) of the
@@ -1018,16 +1021,50 @@ __device__ void coo_pull_phase(const HcArgs &a, int t, const typename VR::T *vre
     if (threadIdx.x <= kMaxPass) s_off[threadIdx.x] = ld_volatile(a.boff + threadIdx.x);
     __syncthreads();
     for (int p = 0; p < a.npass; p++) {
-    // static contiguous slices of bucket p, whole 32*UA steps
+    // static contiguous slices of bucket p, whole 32*UA steps (PICO_PULL_VEC:
+    // steps aligned to 4 arcs, int4 loads, the arcs before bb masked)
     const long long bb = (long long)s_off[p], be = (long long)s_off[p + 1];
-    const long long steps = (be - bb + 32 * UA - 1) / (32 * UA);
+    const long long ab = PICO_PULL_VEC ? (bb & ~3ll) : bb;
+    const long long steps = (be - ab + 32 * UA - 1) / (32 * UA);
     const long long s0 = steps * gwarp / nwarps, s1 = steps * (gwarp + 1) / nwarps;
     for (long long st = s0; st < s1; st++) {
-        const long long e0 = bb + st * (32 * UA);
+        const long long e0 = ab + st * (32 * UA);
         int u[UA], v[UA];
         unsigned ru[UA];
         typename VR::T rv[UA];
         long long hb[UA];
+#if PICO_PULL_VEC
+        static_assert(UA == 4, "vector pull loads: 4 arcs per lane");
+        {
+            // lane L loads arcs e0 + 4L .. +3 as one int4 per column, then the
+            // warp transposes so that step q of lane L is arc e0 + 32q + L (the
+            // scalar mapping: consecutive lanes share u, the REDs coalesce)
+            const long long ev = e0 + 4 * lane;
+            int4 su = make_int4(-1, -1, -1, -1), sv = make_int4(0, 0, 0, 0);
+            const bool vok = ((reinterpret_cast<unsigned long long>(a.pdst) | reinterpret_cast<unsigned long long>(a.psrc)) & 15) == 0;
+            if (vok && ev + 3 < be && ev >= bb) {
+                su = __ldcs(reinterpret_cast<const int4 *>(a.psrc + ev));
+                sv = __ldcs(reinterpret_cast<const int4 *>(a.pdst + ev));
+            } else {
+                int *pu = &su.x, *pv = &sv.x;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const long long e = ev + j;
+                    if (e >= bb && e < be) { pu[j] = __ldcs(a.psrc + e); pv[j] = __ldcs(a.pdst + e); }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UA; q++) {
+                const int src = q * 8 + (lane >> 2), j = lane & 3;
+                const int u0 = __shfl_sync(FULL, su.x, src), u1 = __shfl_sync(FULL, su.y, src);
+                const int u2 = __shfl_sync(FULL, su.z, src), u3 = __shfl_sync(FULL, su.w, src);
+                const int v0 = __shfl_sync(FULL, sv.x, src), v1 = __shfl_sync(FULL, sv.y, src);
+                const int v2 = __shfl_sync(FULL, sv.z, src), v3 = __shfl_sync(FULL, sv.w, src);
+                u[q] = j == 0 ? u0 : j == 1 ? u1 : j == 2 ? u2 : u3;
+                v[q] = j == 0 ? v0 : j == 1 ? v1 : j == 2 ? v2 : v3;
+            }
+        }
+#else
 #pragma unroll
         for (int q = 0; q < UA; q++) {
             long long e = e0 + q * 32 + lane;
@@ -1035,6 +1072,7 @@ __device__ void coo_pull_phase(const HcArgs &a, int t, const typename VR::T *vre
             u[q] = ok ? ld_stream(a.psrc + e, cold) : -1;
             v[q] = ok ? ld_stream(a.pdst + e, cold) : 0;
         }
+#endif
 #pragma unroll
         for (int q = 0; q < UA; q++) {
             ru[q] = u[q] >= 0 ? ld_rec(a.rec + u[q], hot) : 0u;
@@ -1624,10 +1662,35 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
             int per = std::max(1, occ);
             int blocks = sms * per;
             void *args[] = {&a};
+            // PICO_F_L2_PERSIST (A/B): the push rounds' gather target e16 as a
+            // persisting L2 access-policy window for the round kernel
+            const bool persist = (flags & PICO_F_L2_PERSIST) && n > 0;
+            if (persist) {
+                int maxp = 0, maxw = 0;
+                cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev.device);
+                cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev.device);
+                const size_t bytes = std::min<size_t>(sizeof(unsigned short) * (size_t)n, (size_t)maxw);
+                const size_t keep = std::min<size_t>(bytes, (size_t)maxp);
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep);
+                cudaStreamAttrValue v{};
+                v.accessPolicyWindow.base_ptr = a.e16;
+                v.accessPolicyWindow.num_bytes = bytes;
+                v.accessPolicyWindow.hitRatio = bytes ? (float)keep / (float)bytes : 0.f;
+                v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+            }
             tm.start(PICO_K_ROUNDS);
             err = cudaLaunchCooperativeKernel((const void *)hc_rounds_kernel<STATS>, blocks, 512, args, 0, s);
             tm.stop();
             launches++;
+            if (persist) {  // back to the default policy (the limit is process-wide state)
+                cudaStreamAttrValue v{};
+                v.accessPolicyWindow.num_bytes = 0;
+                cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+                cudaCtxResetPersistingL2Cache();
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+            }
             if (err) return err;
             unsigned long long devrounds = 0;
             int derr = 0;
