@@ -487,13 +487,16 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
 // whose h-index may exceed the cap go to the global-bin fallback (GLOBAL=true
 // runs the same procedure on the vertex's own 2m-slot region in HBM).
 // ---------------------------------------------------------------------------
+// cap: the shared-memory bin cap (class C: c_bins; the fallback's first try:
+// the big shared-memory tier).  Returns false (nothing written) when the
+// h-index may exceed the cap: the caller redoes v with more bins.
 template <bool GLOBAL, bool STATS>
-__device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
+__device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int cap) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = lane_id(), wid = tid >> 5, nwarp = nt >> 5;
     long long hb = a.rp[v];
     int d = (int)(a.rp[v + 1] - hb);
-    int B = GLOBAL ? d : min(d, a.tn.c_bins);
+    int B = GLOBAL ? d : min(d, cap);
     if (GLOBAL) bins = a.histo + hb - 1;  // bin b at slot hb + b - 1
     for (int b = tid; b <= B; b += nt)
         if (!GLOBAL || b >= 1) bins[b] = 0;
@@ -545,13 +548,9 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
     __syncthreads();
     int hs = red[33];
     if (!GLOBAL && h == B && d > B) {
-        // the cap may hide a larger h-index: redo with global bins
-        if (tid == 0) {
-            unsigned long long i = atomicAdd(&a.ctl->nX, 1ull);
-            a.F[i] = v;
-        }
+        // the cap may hide a larger h-index: the caller redoes v with more bins
         __syncthreads();
-        return;
+        return false;
     }
     if (GLOBAL) {
         if (tid == 0) a.histo[hb + h - 1] = hs;  // bins 1..h-1 already exact
@@ -584,6 +583,7 @@ __device__ void cta_init_vertex(const HcArgs &a, int v, int *bins, int *red) {
         for (int s2 = tid; s2 < nseg; s2 += nt) a.S[base + s2] = make_int2(v, s2);
     }
     __syncthreads();
+    return true;
 }
 
 template <bool STATS>
@@ -593,17 +593,27 @@ __global__ void __launch_bounds__(512) hc_init_cta_kernel(HcArgs a) {
     const long long nC = (long long)bcast_u64(&a.ctl->nC);
     for (long long idx = blockIdx.x; idx < nC; idx += gridDim.x) {
         int v = a.BC[a.n - 1 - idx];
-        cta_init_vertex<false, STATS>(a, v, bins, red);
+        if (!cta_init_vertex<false, STATS>(a, v, bins, red, a.tn.c_bins) && threadIdx.x == 0) {
+            unsigned long long i = atomicAdd(&a.ctl->nX, 1ull);  // to the fallback
+            a.F[i] = v;
+        }
     }
 }
 
+// the class-C vertices whose h-index reached c_bins (the hubs): first with the
+// big shared-memory tier (one 1024-thread CTA per SM, `big` bins: at RMAT-26
+// every hub fits, its degree h-index is below 45 K), else with global bins in
+// the vertex's own histogram slots (contended HBM atomics on its low bins:
+// 3.2 ms for 352 hubs at RMAT-26 when this was the only fallback)
 template <bool STATS>
-__global__ void __launch_bounds__(512) hc_init_fallback_kernel(HcArgs a) {
+__global__ void __launch_bounds__(1024, 1) hc_init_fallback_kernel(HcArgs a, int big) {
+    extern __shared__ int bins[];
     __shared__ int red[40];
     const long long nX = (long long)bcast_u64(&a.ctl->nX);
     for (long long idx = blockIdx.x; idx < nX; idx += gridDim.x) {
         int v = a.F[idx];
-        cta_init_vertex<true, STATS>(a, v, nullptr, red);
+        if (big == 0 || !cta_init_vertex<false, STATS>(a, v, bins, red, big))
+            cta_init_vertex<true, STATS>(a, v, nullptr, red, 0);
     }
 }
 
@@ -1605,7 +1615,22 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                              (int)smC);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, hc_init_cta_kernel<STATS>, 512, smC);
         hc_init_cta_kernel<STATS><<<sms * std::max(1, occC), 512, smC, s>>>(a);
-        hc_init_fallback_kernel<STATS><<<sms, 512, 0, s>>>(a);
+        {
+            // big shared-memory tier of the fallback: as many bins as fit
+            int maxsm = 0;
+            cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev.device);
+            int big = (flags & PICO_F_TINY_TILES) ? 2 * tn.c_bins : (maxsm - 1024) / (int)sizeof(int) - 1;
+            big = std::max(big, 0);
+            const size_t smF = sizeof(int) * (size_t)(big + 1);
+            if (big > tn.c_bins &&
+                cudaFuncSetAttribute(hc_init_fallback_kernel<STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smF) == cudaSuccess) {
+                hc_init_fallback_kernel<STATS><<<sms, 1024, smF, s>>>(a, big);
+            } else {
+                cudaGetLastError();
+                hc_init_fallback_kernel<STATS><<<sms, 1024, 0, s>>>(a, 0);
+            }
+        }
         int nb = (int)std::min<long long>((n + 255) / 256, (long long)sms * 8);
         hc_shadow_kernel<<<std::max(nb, 1), 256, 0, s>>>(a);
         launches += 5;
@@ -2166,7 +2191,7 @@ cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed) {
         cudaFuncSetAttribute(hc_init_cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, hc_init_cta_kernel<false>, 512, smC);
         hc_init_cta_kernel<false><<<sms * std::max(1, occC), 512, smC, s>>>(a);
-        hc_init_fallback_kernel<false><<<sms, 512, 0, s>>>(a);
+        hc_init_fallback_kernel<false><<<sms, 1024, 0, s>>>(a, 0);
         hc_shadow_kernel<<<grid(h->nloc), 256, 0, s>>>(a);
     }
     a.nv8 = a.c8;
