@@ -18,6 +18,34 @@ import time
 import numpy as np
 
 
+def fixed_point_violations(rp_l, ci_l, vb: int, core, chunk: int = 1 << 27) -> int:
+    """Rows of this rank whose estimate is not the h-index of its neighbours'
+    (P:138-146: #nbrs with core >= c is >= c and #nbrs with core >= c+1 is <
+    c+1), or that break 0 <= core <= deg / core = 0 iff deg = 0.
+    Chunked over the rank's arcs (torch, on the rank's GPU)."""
+    import torch
+    nloc = rp_l.numel() - 1
+    if nloc == 0:
+        return 0
+    deg = rp_l[1:] - rp_l[:-1]
+    cv = core[vb:vb + nloc].to(torch.int64)
+    bad = int(((cv < 0) | (cv > deg) | ((cv == 0) != (deg == 0))).sum().item())
+    ge = torch.zeros(nloc, dtype=torch.int64, device=core.device)
+    gt = torch.zeros(nloc, dtype=torch.int64, device=core.device)
+    arcs = ci_l.numel()
+    for a0 in range(0, arcs, chunk):
+        a1 = min(arcs, a0 + chunk)
+        rows = torch.searchsorted(rp_l, torch.arange(a0, a1, device=core.device, dtype=torch.int64), right=True) - 1
+        cu = core[ci_l[a0:a1].to(torch.int64)].to(torch.int64)
+        c = cv[rows]
+        ge += torch.bincount(rows, weights=(cu >= c).to(torch.float64), minlength=nloc).to(torch.int64)
+        gt += torch.bincount(rows, weights=(cu >= c + 1).to(torch.float64), minlength=nloc).to(torch.int64)
+        del rows, cu, c
+    live = deg > 0
+    bad += int((live & ((ge < cv) | (gt >= cv + 1))).sum().item())
+    return bad
+
+
 def bench_sharded(args):
     import torch
     import torch.distributed as dist
@@ -41,11 +69,32 @@ def bench_sharded(args):
     ex = sharded.TorchDistExchange()
     stream = torch.cuda.current_stream(dev)
 
-    cfg, rp, ci = bench.build_graph(args.config, dev)
-    n, m = rp.numel() - 1, ci.numel() // 2
-    bounds = sharded.partition(rp, world)
-    vb, ve = bounds[rank], bounds[rank + 1]
-    rp_l, ci_l = sharded.local_rows(rp, ci, vb, ve)
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    per_rank = not cfg.compact  # uncompacted recipes (T, C5, C1): each rank generates only its rows
+    rp = ci = None
+    t_gen = time.time()
+    if per_rank:
+        n = cfg.n
+        bounds = sharded.partition_vertices(n, world)
+        vb, ve = bounds[rank], bounds[rank + 1]
+        rp_l, ci_l = cfg.build_rows(vb, ve, device=dev)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        arcs_t = torch.tensor([ci_l.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(arcs_t)
+        m = int(arcs_t.item()) // 2
+        gen_note = "per rank: each GPU generated only its own rows (equal vertex ranges)"
+    else:
+        cfg, rp, ci = bench.build_graph(args.config, dev)
+        n, m = rp.numel() - 1, ci.numel() // 2
+        bounds = sharded.partition(rp, world)
+        vb, ve = bounds[rank], bounds[rank + 1]
+        rp_l, ci_l = sharded.local_rows(rp, ci, vb, ve)
+        gen_note = "whole graph on every rank (compaction renumbers globally), arc-balanced ranges"
+    t_gen = time.time() - t_gen
+    if rank == 0:
+        bench.log(f"[bench-sharded] {args.config}: n={n} m={m} local arcs {ci_l.numel()} generated in {t_gen:.1f}s ({gen_note})")
 
     comm, exchange_note = None, "torch.distributed"
     if args.exchange == "nccl":
@@ -115,21 +164,32 @@ def bench_sharded(args):
     ms = ex.max_over_ranks(ms_rank, dev)
 
     # parity: the assembled coreness against the single-GPU path (itself
-    # bit-exact vs the oracle in tests and in the N=1 bench) on rank 0
+    # bit-exact vs the oracle in tests and in the N=1 bench) on rank 0, where
+    # the whole graph fits one GPU; always, on every rank, the h-index fixed
+    # point of its own rows against the assembled vector
     counts = ex.allgather_counts(run.core_local.numel(), dev)
     core = ex.allgatherv(run.core_local, counts)
-    parity = "skipped"
-    if rank == 0:
-        ref = pico.coreness(rp, ci)
-        parity = "bit-exact vs single-GPU" if torch.equal(core, ref) else "MISMATCH"
+    fp_bad = fixed_point_violations(rp_l, ci_l, vb, core)
+    fp_bad = int(ex.max_over_ranks(float(fp_bad), dev))
+    parity = f"h-index fixed point on every rank's rows: {'ok' if fp_bad == 0 else f'{fp_bad} violations'}"
+    ref_stats = None
+    if rank == 0 and n <= (1 << 27):
+        if rp is None:
+            rp, ci = cfg.build(device=dev)
+        ref_stats = pico.Stats()
+        ref_fs = np.zeros(1 << 16, dtype=np.int64)
+        ref_ra = np.zeros(1 << 16, dtype=np.int64)
+        ref = pico.coreness(rp, ci, flags=pico.F_STATS, stats=ref_stats, frontier_sizes=ref_fs, round_arcs=ref_ra)
+        parity = ("bit-exact vs single-GPU" if torch.equal(core, ref) else "MISMATCH vs single-GPU") + "; " + parity
         if not args.no_oracle and n * 1 <= (8 << 20):
             import oracle
-            import synth
             r_np, c_np = synth.to_numpy(rp, ci)
             if np.array_equal(oracle.bz(r_np, c_np), core.cpu().numpy()):
-                parity = "bit-exact vs oracle"
+                parity = "bit-exact vs oracle; " + parity
             else:
-                parity = "MISMATCH vs oracle"
+                parity = "MISMATCH vs oracle; " + parity
+        del rp, ci
+        torch.cuda.empty_cache()
 
     # e2e: local rows from pinned host memory -> device, sharded run, result
     # back to pinned host memory, per step
@@ -150,6 +210,32 @@ def bench_sharded(args):
 
     if rank == 0:
         peak, src = bench.hbm_peak()
+        # roofline: the method's bytes of the whole graph (identical rounds and
+        # frontiers at every P; counted by a single-GPU STATS run where the
+        # graph fits one GPU) over the max-over-ranks step time and N peaks
+        roof = {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
+                "traffic": None, "peak_source": src + f" x {world} GPUs", "kernel": "whole sharded step"}
+        if ref_stats is not None and not peel:
+            sd = ref_stats.to_dict()
+            b = bench.hc_bytes(n, m, sd, int(ref_fs[0]), int(ref_ra[:sd["rounds"]].sum()))
+            tot = sum(b.values())
+            roof.update({"achieved": tot / (ms * 1e-3) / 1e9, "frac": tot / (ms * 1e-3) / 1e9 / (peak * world),
+                         "alg_bytes": b})
+        else:
+            roof["note"] = "method bytes need a single-GPU STATS run, which does not fit one GPU here"
+        # cpu_baseline: the oracle on this host, one core, on the reference
+        # arm's bounded sample of the workload
+        cpu_base = None
+        if not args.no_oracle:
+            import oracle
+            _, rp_s, ci_s, what = bench.reference_graph(args.config, dev)
+            r_np, c_np = synth.to_numpy(rp_s, ci_s)
+            del rp_s, ci_s
+            _, times = bench.oracle_baseline(r_np, c_np, budget_s=10.0, max_runs=3)
+            tb = min(times)
+            cpu_base = {"value": (c_np.size // 2) / tb, "unit": bench.UNIT, "cores": 1, "kind": "oracle",
+                        "sample": f"{what} (n={r_np.size - 1}, m={c_np.size // 2}), serial BZ, best of {len(times)}",
+                        "ms": 1e3 * tb}
         launches = (8 + 3 * run.subrounds + 3 * run.levels) if peel else 12 + 4 * run.rounds
         if peel:
             iters = {"peelone_levels": run.levels, "peelone_subrounds": run.subrounds, "kmax": run.kmax}
@@ -167,12 +253,10 @@ def bench_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": cfg.note, "config": args.config, "algo": f"{args.algo}-sharded", "n": n, "m": m,
-                       "parallelism": par,
+                       "parallelism": par, "generation": gen_note,
                        "l2_flush": "inputs larger than L2"},
-            "roofline": {"bound": "hbm", "achieved": None, "peak": peak * world, "unit": "GB/s", "frac": None,
-                         "traffic": None, "peak_source": src + f" x {world} GPUs",
-                         "note": "per-kernel sharded timings not instrumented; see the N=1 line"},
-            "cpu_baseline": None,
+            "roofline": roof,
+            "cpu_baseline": cpu_base,
             "e2e": {"value": m / e2e_t, "unit": bench.UNIT, "ms_per_step": 1e3 * e2e_t,
                     "h2d_bytes_per_step": int(8 * n + 4 * 2 * m), "d2h_bytes_per_step": int(4 * n)},
             "gpu_launches": launches * args.steps * world,

@@ -45,6 +45,14 @@ def partition(rowptr, nparts: int) -> list[int]:
     return bounds
 
 
+def partition_vertices(n: int, nparts: int) -> list[int]:
+    """Equal vertex ranges [n r / P, n (r+1) / P): the partition of a run whose
+    ranks generate only their own rows (no global rowptr to balance arcs on;
+    the generators' seeded relabel spreads the hubs, so the ranges' arc counts
+    are balanced in expectation)."""
+    return [n * r // nparts for r in range(nparts + 1)]
+
+
 def local_rows(rowptr, colidx, vb: int, ve: int):
     """Rows [vb, ve) as (rowptr_local with rowptr_local[0] = 0, colidx_local)."""
     a, b = int(rowptr[vb]), int(rowptr[ve])

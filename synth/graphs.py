@@ -131,9 +131,9 @@ def _relabel_perm(n: int, seed: int, device) -> torch.Tensor:
 
 
 def rmat_edges(scale: int, samples: int, abcd=(0.57, 0.19, 0.19, 0.05), seed: int = 1,
-               noise: float = 0.0, device="cpu", chunk: int = 1 << 25):
+               noise: float = 0.0, device="cpu", chunk: int = 1 << 25, first: int = 0):
     """Raw RMAT/Kronecker samples (src, dst) as int64 tensors (before the
-    relabel/symmetrize/dedup steps)."""
+    relabel/symmetrize/dedup steps): samples first .. first+samples-1."""
     a, b, c, d = abcd
     tot = a + b + c + d
     a, b, c = a / tot, b / tot, c / tot
@@ -156,8 +156,8 @@ def rmat_edges(scale: int, samples: int, abcd=(0.57, 0.19, 0.19, 0.05), seed: in
         t3 = int((aa + bb + cc) * 4294967296.0)
         thr.append((t1, t2, t3))
     srcs, dsts = [], []
-    for start in range(0, samples, chunk):
-        cnt = min(chunk, samples - start)
+    for start in range(first, first + samples, chunk):
+        cnt = min(chunk, first + samples - start)
         idx = torch.arange(start, start + cnt, dtype=torch.int64, device=device)
         s = torch.zeros(cnt, dtype=torch.int64, device=device)
         t = torch.zeros(cnt, dtype=torch.int64, device=device)
@@ -192,6 +192,53 @@ def rmat(scale: int, edge_factor: float = 16, abcd=(0.57, 0.19, 0.19, 0.05), see
     if compact:
         rp, ci = compact_isolated(rp, ci)
     return rp, ci
+
+
+def rmat_rows(scale: int, vb: int, ve: int, edge_factor: float = 16, abcd=(0.57, 0.19, 0.19, 0.05),
+              seed: int = 1, noise: float = 0.0, samples: int | None = None, device="cpu",
+              chunk: int = 1 << 25):
+    """Rows [vb, ve) of ``rmat(...)`` (compact=False) without building the rest:
+    (rowptr_local int64[ve-vb+1] with rowptr_local[0] = 0, colidx_local int32
+    with global ids) -- the same arrays as slicing the full CSR, generated by
+    one rank of a sharded run (C5: RMAT-30, 33 G arcs, 1/P per GPU).  Every
+    rank draws all samples (counter-based, so identical on every rank), maps
+    them through the seeded relabel, symmetrizes, keeps the arcs whose source
+    it owns, then sorts and dedups its own rows."""
+    n = 1 << scale
+    if samples is None:
+        samples = int(edge_factor * n)
+    nloc = ve - vb
+    perm = _relabel_perm(n, seed, device).to(torch.int32 if n <= (1 << 31) else torch.int64)
+    keys = []
+    for start in range(0, samples, chunk):
+        cnt = min(chunk, samples - start)
+        s, t = rmat_edges(scale, cnt, abcd, seed, noise, device, chunk=cnt, first=start)
+        s = perm[s].to(torch.int64)
+        t = perm[t].to(torch.int64)
+        keep = s != t
+        s, t = s[keep], t[keep]
+        for a, b in ((s, t), (t, s)):  # both arc directions of each edge
+            own = (a >= vb) & (a < ve)
+            keys.append(((a[own] - vb) << 31) | b[own])
+        del s, t, keep
+    del perm
+    keys = torch.cat(keys) if keys else torch.zeros(0, dtype=torch.int64, device=device)
+    counts = torch.zeros(nloc, dtype=torch.int64, device=device)
+    cols = []
+    nparts = max(1, -(-keys.numel() // (_SORT_LIM // 2)))
+    for q in range(nparts):  # sorted in local row ranges (torch.sort takes < 2^31 items)
+        lo, hi = nloc * q // nparts, nloc * (q + 1) // nparts
+        part = keys if nparts == 1 else keys[(keys >= (lo << 31)) & (keys < (hi << 31))]
+        part = torch.unique_consecutive(torch.sort(part).values)
+        rows = part >> 31
+        cols.append((part & ((1 << 31) - 1)).to(torch.int32))
+        counts += torch.bincount(rows, minlength=nloc)
+        del part, rows
+    del keys
+    colidx = cols[0] if len(cols) == 1 else torch.cat(cols)
+    rowptr = torch.zeros(nloc + 1, dtype=torch.int64, device=device)
+    rowptr[1:] = torch.cumsum(counts, 0)
+    return rowptr, colidx
 
 
 def erdos_renyi(n: int, p: float, seed: int = 1, device="cpu"):
@@ -285,6 +332,19 @@ class GraphConfig:
     def build(self, device="cpu"):
         return rmat(self.scale, abcd=self.abcd, seed=self.seed, noise=self.noise,
                     compact=self.compact, samples=self.samples, device=device)
+
+    @property
+    def n(self) -> int:
+        """Vertex count of an uncompacted config (compacted ones: known after the build)."""
+        return 1 << self.scale
+
+    def build_rows(self, vb: int, ve: int, device="cpu"):
+        """Rows [vb, ve) only (one rank of a sharded run); uncompacted configs
+        (compaction renumbers globally)."""
+        if self.compact:
+            raise ValueError(f"{self.name} is compacted: build it whole and slice")
+        return rmat_rows(self.scale, vb, ve, abcd=self.abcd, seed=self.seed, noise=self.noise,
+                         samples=self.samples, device=device)
 
 
 CONFIGS = {

@@ -53,6 +53,24 @@ def test_local_rows_slices():
     assert total == ci.numel()
 
 
+@pytest.mark.parametrize("cfg", ["R12", "C1"])
+def test_rows_generation_matches_slices(cfg):
+    """Per-rank generation (synth rmat_rows, used by the sharded bench so that
+    C5 = RMAT-30 never exists whole on one GPU) gives exactly the rows of the
+    full graph: equal vertex ranges at P = 1, 3, 4."""
+    c = synth.CONFIGS[cfg]
+    rp, ci = c.build()
+    n = rp.numel() - 1
+    for parts in (1, 3, 4):
+        b = sharded.partition_vertices(n, parts)
+        for r in range(parts):
+            rl, cl = c.build_rows(b[r], b[r + 1])
+            el, ecl = sharded.local_rows(rp, ci, b[r], b[r + 1])
+            assert torch.equal(rl, el) and torch.equal(cl, ecl), (cfg, parts, r)
+    with pytest.raises(ValueError):
+        synth.CONFIGS["C2"].build_rows(0, 10)  # compacted configs renumber globally
+
+
 # ------------------------------------------------- mock shard (test only)
 class JacobiShard:
     """Owned vertices [vb, ve): synchronous Index2core on a replica of every
