@@ -190,6 +190,10 @@ typedef struct {
     int64_t *round_ns;
     /* the algorithm that ran (PICO_ALGO_AUTO resolved) */
     int64_t algo;
+    /* pico_dyn_insert_edges: vertices whose estimate was raised (the band-
+     * restricted BFS set R) and that BFS's levels */
+    int64_t affected;
+    int64_t bfs_levels;
 } pico_stats_t;
 
 /* The north-star entry point: coreness of every vertex, device buffers. */

@@ -21,8 +21,13 @@
  *    loop or an id out of range -> PICO_EINVAL, detected before anything is
  *    modified: the handle keeps the previous graph and stays usable.
  *  - Calls are blocking and ordered on the stream given at creation.
- *  - Insertions are not supported (they can raise coreness, which the
- *    decreasing Index2core iteration cannot follow from the current state).
+ *  - Insertions (pico_dyn_insert_edges) can raise coreness, by at most one
+ *    per inserted edge and only inside the band of old coreness values the
+ *    batch touches: the handle raises the estimates of the vertices the band-
+ *    restricted BFS from the new edges reaches to an upper bound
+ *    min(deg, core + k), rebuilds its CSR with the new arcs, and reruns the
+ *    rounds warm-started from those estimates (DESIGN.md "Incremental
+ *    HistoCore").
  */
 #ifndef PICO_DYN_H_
 #define PICO_DYN_H_
@@ -47,6 +52,15 @@ int pico_dyn_coreness(pico_dyn_t h, int32_t *core_out);
  * (optional): rounds of the update and, with frontier_sizes set, |C_t| of
  * each. */
 int pico_dyn_delete_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, int64_t k, pico_stats_t *stats);
+
+/* Insert k undirected edges {src[i], dst[i]} (DEVICE int32 arrays) and
+ * bring the coreness up to date.  The batch is canonicalised as for
+ * deletions (repeated edges count once); a self loop, an id out of range or
+ * an edge already in the graph -> PICO_EINVAL before anything is modified.
+ * Cost: O(m) to rebuild the handle's CSR and histograms, plus the rounds
+ * from the raised estimates.  stats (optional): the warm-started run's
+ * counters; .affected = vertices whose estimate was raised, .bfs_levels. */
+int pico_dyn_insert_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, int64_t k, pico_stats_t *stats);
 
 int pico_dyn_destroy(pico_dyn_t h);
 

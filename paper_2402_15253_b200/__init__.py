@@ -178,6 +178,14 @@ class DynamicCoreness:
         return out
 
     def delete_edges(self, src, dst, stats: Stats | None = None, frontier_sizes=None):
+        """Delete undirected edges {src[i], dst[i]} (pico_dyn_delete_edges)."""
+        return self._update(self.lib.pico_dyn_delete_edges, src, dst, stats, frontier_sizes)
+
+    def insert_edges(self, src, dst, stats: Stats | None = None, frontier_sizes=None):
+        """Insert undirected edges {src[i], dst[i]} (pico_dyn_insert_edges)."""
+        return self._update(self.lib.pico_dyn_insert_edges, src, dst, stats, frontier_sizes)
+
+    def _update(self, fn, src, dst, stats, frontier_sizes):
         import torch
         if src.numel() != dst.numel():
             raise ValueError(f"src and dst must have the same length ({src.numel()} != {dst.numel()})")
@@ -191,9 +199,8 @@ class DynamicCoreness:
             _host_i64("frontier_sizes", frontier_sizes)
             st.frontier_sizes = frontier_sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
             st.frontier_sizes_cap = frontier_sizes.size
-        check(self.lib.pico_dyn_delete_edges(self.h, src.data_ptr() if src.numel() else None,
-                                             dst.data_ptr() if dst.numel() else None, src.numel(),
-                                             ctypes.byref(st) if st is not None else None))
+        check(fn(self.h, src.data_ptr() if src.numel() else None, dst.data_ptr() if dst.numel() else None,
+                 src.numel(), ctypes.byref(st) if st is not None else None))
         return st
 
     def close(self):

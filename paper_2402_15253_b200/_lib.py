@@ -66,11 +66,15 @@ class Stats(ctypes.Structure):
         ("round_arcs", ctypes.POINTER(ctypes.c_int64)),
         ("round_ns", ctypes.POINTER(ctypes.c_int64)),
         ("algo", ctypes.c_int64),
+        ("affected", ctypes.c_int64),
+        ("bfs_levels", ctypes.c_int64),
     ]
 
     def to_dict(self) -> dict:
         d = {k: int(getattr(self, k)) for k, _ in self._fields_[:16]}
         d["algo"] = int(self.algo)
+        d["affected"] = int(self.affected)
+        d["bfs_levels"] = int(self.bfs_levels)
         d["kernel_ms"] = {K_NAMES[i]: float(self.kernel_ms[i]) for i in range(9) if self.kernel_launches[i]}
         d["kernel_launches"] = {K_NAMES[i]: int(self.kernel_launches[i]) for i in range(9) if self.kernel_launches[i]}
         return d
@@ -130,6 +134,8 @@ def load(path: str | None = None):
     lib.pico_dyn_coreness.restype = i32
     lib.pico_dyn_delete_edges.argtypes = [vp, vp, vp, i64, ctypes.POINTER(Stats)]
     lib.pico_dyn_delete_edges.restype = i32
+    lib.pico_dyn_insert_edges.argtypes = [vp, vp, vp, i64, ctypes.POINTER(Stats)]
+    lib.pico_dyn_insert_edges.restype = i32
     lib.pico_dyn_destroy.argtypes = [vp]
     lib.pico_dyn_destroy.restype = i32
     _lib = lib

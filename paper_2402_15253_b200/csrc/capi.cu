@@ -961,6 +961,16 @@ int pico_dyn_delete_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, 
     return e ? cuda_fail(e, "dyn delete") : PICO_OK;
 }
 
+int pico_dyn_insert_edges(pico_dyn_t h, const int32_t *src, const int32_t *dst, int64_t k, pico_stats_t *stats) {
+    g_last_error.clear();
+    reset_stats(stats);
+    if (!h || k < 0 || (k > 0 && (!src || !dst))) return fail(PICO_EINVAL, "bad argument");
+    cudaError_t e = dyn_insert(h->impl, src, dst, k, stats);
+    if (e == cudaErrorInvalidValue)
+        return fail(PICO_EINVAL, "an inserted edge is already in the graph (or a self loop / bad id)");
+    return e ? cuda_fail(e, "dyn insert") : PICO_OK;
+}
+
 int pico_dyn_destroy(pico_dyn_t h) {
     g_last_error.clear();
     if (!h) return PICO_OK;

@@ -137,6 +137,11 @@ struct HcArgs {
     // decremental updates (pico_dyn_*): a vertex that lost every neighbour
     // walks down to h = 0 instead of flagging a broken invariant
     int allow_zero;
+    // warm start (edge insertions, pico_dyn_insert_edges): the round-0
+    // estimates (an upper bound of the coreness, <= deg) instead of the
+    // degrees: InitHisto caps v's histogram at h0[v] and bins neighbours by
+    // min(h0[u], h0[v]); null = the degrees
+    const int *h0;
     int *psrc, *pdst;
 };
 
@@ -350,6 +355,7 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
         }
         bool mine = valid && d >= 1 && d <= a.tn.a_max;
         int nseg = 0, h = 0;
+        const int cap = (mine && a.h0) ? min(__ldg(a.h0 + v), d) : d;  // the round-0 estimate
         if (mine) {
             int cnt[NB];
 #pragma unroll
@@ -357,14 +363,14 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
             for (int e = 0; e < d; e++) {
                 int u = ld_stream(a.ci + hb + e, cold);
                 if (a.prefilter) a.ro[hb + e] = u;  // short rows: copied in order
-                int x = init_val_small(a, u, d, hot);  // min(core[u], core[v])
+                int x = init_val_small(a, u, cap, hot);  // min(core[u], core[v])
 #pragma unroll
                 for (int b = 0; b < NB; b++) cnt[b] += (x == b + 1);
             }
             int s = 0, hs = 0;
 #pragma unroll
             for (int b = NB; b >= 1; b--) {
-                if (b <= d && h == 0) {
+                if (b <= cap && h == 0) {
                     s += cnt[b - 1];
                     if (s >= b) { h = b; hs = s; }
                 }
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(256) hc_init_small_kernel(HcArgs a) {
                 else if (b == h) a.histo[hb + b - 1] = hs;
             }
             a.core[v] = h;
-            if (h < d) {
+            if (h < cap) {
                 a.slen[v] = d;  // d <= a_max: whole row
                 nseg = nseg_of(d, a.tn.seg);
             }
@@ -421,9 +427,10 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         long long hb = a.rp[v];
         int d = (int)(a.rp[v + 1] - hb);
         if (PART != 0 && (d <= (int)SAT8) != (PART == 1)) continue;  // the other launch's row (warp-uniform)
-        for (int b = lane; b <= d; b += 32) bins[b] = 0;
+        const int cap = a.h0 ? min(__ldg(a.h0 + v), d) : d;  // the round-0 estimate
+        for (int b = lane; b <= cap; b += 32) bins[b] = 0;
         __syncwarp();
-        auto val = [&](int u) { return PART == 1 ? init_val_small(a, u, d, hot) : init_val(a, u, d, hot); };
+        auto val = [&](int u) { return PART == 1 ? init_val_small(a, u, cap, hot) : init_val(a, u, cap, hot); };
         {
             int e = lane;
             for (; e + 96 < d; e += 128) {  // 4 gathers in flight per lane
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         }
         __syncwarp();
         // descending walk for the h-index (SumHisto on the fresh histogram)
-        int carry = 0, top = d, h = 0, hs = 0;
+        int carry = 0, top = cap, h = 0, hs = 0;
         for (;;) {
             int kk = top - lane;
             int val = kk >= 1 ? bins[kk] : 0;
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(256) hc_init_warp_kernel(HcArgs a) {
         }
         for (int b = 1 + lane; b <= h; b += 32) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
         __syncwarp();
-        const bool changed = h < d;
+        const bool changed = h < cap;
         int L = 0;
         if (changed && lane == 0) L = scan_len(a, hb, d, h);
         L = __shfl_sync(FULL, L, 0);
@@ -496,7 +503,8 @@ __device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int
     const int lane = lane_id(), wid = tid >> 5, nwarp = nt >> 5;
     long long hb = a.rp[v];
     int d = (int)(a.rp[v + 1] - hb);
-    int B = GLOBAL ? d : min(d, cap);
+    const int ecap = a.h0 ? min(__ldg(a.h0 + v), d) : d;  // the round-0 estimate
+    int B = GLOBAL ? ecap : min(ecap, cap);
     if (GLOBAL) bins = a.histo + hb - 1;  // bin b at slot hb + b - 1
     for (int b = tid; b <= B; b += nt)
         if (!GLOBAL || b >= 1) bins[b] = 0;
@@ -507,14 +515,14 @@ __device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int
         for (; e + 3 * nt < d; e += 4 * nt) {  // 4 gathers in flight per thread
             int u0 = ld_stream(a.ci + hb + e, cold), u1 = ld_stream(a.ci + hb + e + nt, cold);
             int u2 = ld_stream(a.ci + hb + e + 2 * nt, cold), u3 = ld_stream(a.ci + hb + e + 3 * nt, cold);
-            int x0 = init_val(a, u0, d, hot), x1 = init_val(a, u1, d, hot);
-            int x2 = init_val(a, u2, d, hot), x3 = init_val(a, u3, d, hot);
+            int x0 = init_val(a, u0, ecap, hot), x1 = init_val(a, u1, ecap, hot);
+            int x2 = init_val(a, u2, ecap, hot), x3 = init_val(a, u3, ecap, hot);
             atomicAdd(&bins[min(x0, B)], 1);
             atomicAdd(&bins[min(x1, B)], 1);
             atomicAdd(&bins[min(x2, B)], 1);
             atomicAdd(&bins[min(x3, B)], 1);
         }
-        for (; e < d; e += nt) atomicAdd(&bins[min(init_val(a, ld_stream(a.ci + hb + e, cold), d, hot), B)], 1);
+        for (; e < d; e += nt) atomicAdd(&bins[min(init_val(a, ld_stream(a.ci + hb + e, cold), ecap, hot), B)], 1);
     }
     __syncthreads();
     // block-wide descending search: h = max b in 1..B with sum_{j>=b} bins[j] >= b
@@ -547,7 +555,7 @@ __device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int
     if (cand == h && cand) red[33] = cs;
     __syncthreads();
     int hs = red[33];
-    if (!GLOBAL && h == B && d > B) {
+    if (!GLOBAL && h == B && ecap > B) {
         // the cap may hide a larger h-index: the caller redoes v with more bins
         __syncthreads();
         return false;
@@ -558,7 +566,7 @@ __device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int
         for (int b = 1 + tid; b <= h; b += nt) a.histo[hb + b - 1] = (b < h) ? bins[b] : hs;
     }
     if (tid == 0) {
-        const bool changed = h < d;
+        const bool changed = h < ecap;
         a.core[v] = h;
         int L = changed ? scan_len(a, hb, d, h) : 0;
         int ns = nseg_of(L, a.tn.seg);
@@ -1490,12 +1498,26 @@ struct Timer {
     }
 };
 
+// warm start: the round-0 estimates h0 replace the degrees in the arrays
+// InitHisto gathers (oldcore = the exact value, c8 / c16 its shadows)
+__global__ void hc_h0_kernel(HcArgs a) {
+    long long nthreads = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += nthreads) {
+        const int d = (int)(a.rp[v + 1] - a.rp[v]);
+        const int x = min(a.h0[v], d);
+        a.oldc[v] = x;
+        set_c8(a, (int)v, x);
+    }
+}
+
 template <bool STATS>
 static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, long long arcs,
                             int *core, cudaStream_t s, uint32_t flags, void *ws,
-                            pico_stats_t *st, const DevInfo &dev, HcArgs *keep = nullptr) {
+                            pico_stats_t *st, const DevInfo &dev, HcArgs *keep = nullptr,
+                            const int *h0 = nullptr) {
     HcArgs a;
     a.allow_zero = 0;
+    a.h0 = h0;
     Tune tn = hc_tune(flags);
     HcLayout L = hc_layout(n, arcs, flags);
     char *p = (char *)ws;
@@ -1549,6 +1571,10 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
         int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sms * 16);
         hc_degree_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
         launches++;
+        if (h0 && n > 0) {
+            hc_h0_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+            launches++;
+        }
     }
     tm.stop();
     // the bucketed edge list is built before InitHisto: it borrows the
@@ -2079,6 +2105,7 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     a.pshift = hc_pshift(ng, flags, 8);
     if (L.npass == 1) a.pdst = const_cast<int *>(ci);
     a.prefilter = 0;  // the shard's push UpdateHisto walks the CSC, not the rows
+    a.h0 = nullptr;
     p += align256(L.total);
     h->deg8g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
     h->deg16g = (unsigned short *)p; p += align256(sizeof(unsigned short) * (size_t)ng);
@@ -2523,6 +2550,259 @@ cudaError_t dyn_delete(Dyn *h, const int *src, const int *dst, long long k, pico
                 st->frontier_sizes[i] = sizes[i];
     }
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Edge insertions (pico_dyn_insert_edges).  An insertion can raise coreness, by
+// at most one per inserted edge, and only for vertices whose old coreness lies
+// in the band [Kmin, Kmax] (Kmin = min over the batch of min(core x, core y),
+// Kmax = max of the same + k - 1) that are connected to an inserted endpoint
+// through band vertices (the subcore argument of single-edge insertion,
+// applied edge by edge).  So
+//   1. R = band-restricted BFS from the in-band endpoints,
+//   2. est = min(deg_new, core + k) on R, core elsewhere: an upper bound of
+//      the new coreness that equals it outside R,
+//   3. the CSR is rebuilt with the new arcs (tombstones of earlier deletions
+//      dropped), and HistoCore runs warm-started from est (InitHisto capped at
+//      est, P:496-500 with est for the degrees): the synchronous iteration
+//      from an upper bound converges to the greatest fixed point below it,
+//      the new coreness, and only R and its neighbourhood change.
+// ---------------------------------------------------------------------------
+__global__ void dyn_ins_check_kernel(HcArgs a, const int *ci_own, const unsigned long long *keys, long long k,
+                                     int *err) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = gw; i < k; i += nw) {
+        const unsigned long long key = keys[i];
+        if (key == ~0ull || (i > 0 && keys[i - 1] == key)) continue;
+        const int x = (int)(key >> 32), y = (int)(key & 0xffffffffu);
+        if (dyn_find_arc(a, ci_own, x, y) >= 0 && lane_id() == 0) atomicOr(err, 2);  // already an edge
+    }
+}
+
+__global__ void dyn_ins_band_kernel(const unsigned long long *keys, long long k, const int *core, int *kb) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += nt) {
+        const unsigned long long key = keys[i];
+        if (key == ~0ull) continue;
+        const int c = min(core[(int)(key >> 32)], core[(int)(key & 0xffffffffu)]);
+        atomicMin(kb, c);
+        atomicMax(kb + 1, c);
+    }
+}
+
+__device__ __forceinline__ void dyn_ins_visit(int u, unsigned *vis, int *F, unsigned long long *nF) {
+    const unsigned bit = 1u << (u & 31);
+    if (!(atomicOr(vis + (u >> 5), bit) & bit)) F[atomicAdd(nF, 1ull)] = u;
+}
+
+__global__ void dyn_ins_seed_kernel(const unsigned long long *keys, long long k, const int *core, int kmin, int kmax,
+                                    unsigned *vis, int *F, unsigned long long *nF) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += nt) {
+        const unsigned long long key = keys[i];
+        if (key == ~0ull) continue;
+        for (int e = 0; e < 2; e++) {
+            const int x = e ? (int)(key & 0xffffffffu) : (int)(key >> 32);
+            if (core[x] >= kmin && core[x] <= kmax) dyn_ins_visit(x, vis, F, nF);
+        }
+    }
+}
+
+// one BFS level: warp per frontier vertex, band neighbours not yet visited
+__global__ void dyn_ins_bfs_kernel(const long long *rp, const int *ci, const int *core, int kmin, int kmax,
+                                   unsigned *vis, const int *F, long long nf, int *Fn, unsigned long long *nFn) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = gw; i < nf; i += nw) {
+        const int v = F[i];
+        for (long long e = rp[v] + lane_id(); e < rp[v + 1]; e += 32) {
+            const int u = ci[e];
+            if (u != v && core[u] >= kmin && core[u] <= kmax) dyn_ins_visit(u, vis, Fn, nFn);  // u == v: tombstone
+        }
+    }
+}
+
+// live degree (tombstones of deletions are self-loops) + inserted arcs
+__global__ void dyn_ins_deg_kernel(const long long *rp, const int *ci, long long n, long long *deg) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long v = gw; v < n; v += nw) {
+        long long c = 0;
+        for (long long e = rp[v] + lane_id(); e < rp[v + 1]; e += 32) c += ci[e] != (int)v;
+        c = warp_sum64(c);
+        if (lane_id() == 0) deg[v] = c;
+    }
+}
+
+__global__ void dyn_ins_keys_kernel(const long long *rp, const int *ci, long long n, long long arcs,
+                                    const unsigned long long *ikeys, long long k, long long *deg,
+                                    unsigned long long *keys) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long v = gw; v < n; v += nw)  // the live arcs, at their old positions
+        for (long long e = rp[v] + lane_id(); e < rp[v + 1]; e += 32) {
+            const int u = ci[e];
+            keys[e] = u != (int)v ? ((unsigned long long)v << 32) | (unsigned)u : ~0ull;
+        }
+    const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = gt; i < k; i += nt) {  // both arcs of each new edge, after them
+        const unsigned long long key = ikeys[i];
+        const bool ok = key != ~0ull && !(i > 0 && ikeys[i - 1] == key);
+        const unsigned x = (unsigned)(key >> 32), y = (unsigned)(key & 0xffffffffu);
+        keys[arcs + 2 * i] = ok ? ((unsigned long long)x << 32) | y : ~0ull;
+        keys[arcs + 2 * i + 1] = ok ? ((unsigned long long)y << 32) | x : ~0ull;
+        if (ok) {
+            atomicAdd((unsigned long long *)(deg + x), 1ull);
+            atomicAdd((unsigned long long *)(deg + y), 1ull);
+        }
+    }
+}
+
+__global__ void dyn_ins_est_kernel(const int *core, const unsigned *vis, const long long *rp_new, long long n,
+                                   long long k, int *est) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nt) {
+        const long long d = rp_new[v + 1] - rp_new[v];
+        const bool r = (vis[v >> 5] >> (v & 31)) & 1u;
+        est[v] = r ? (int)min(d, (long long)core[v] + k) : core[v];
+    }
+}
+
+__global__ void dyn_ins_cols_kernel(const unsigned long long *keys, long long arcs, int *ci) {
+    long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < arcs; i += nt)
+        ci[i] = (int)(keys[i] & 0xffffffffu);
+}
+
+// returns cudaErrorInvalidValue for a self loop, an id out of range or an
+// edge that is already in the graph (nothing modified)
+cudaError_t dyn_insert(Dyn *h, const int *src, const int *dst, long long k, pico_stats_t *st) {
+    cudaStream_t s = h->s;
+    const int sms = h->dev.sms;
+    const long long n = h->n;
+    cudaError_t e = cudaSuccess;
+    if (k <= 0) return cudaSuccess;
+    // --- canonical sorted keys, checked before anything is modified
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys((void *)nullptr, tb, (const unsigned long long *)nullptr,
+                                   (unsigned long long *)nullptr, k);
+    const size_t kb = align256(sizeof(unsigned long long) * (size_t)k);
+    char *buf = nullptr;
+    if ((e = lib_malloc_async(&buf, 2 * kb + align256(tb) + 256, s))) return e;
+    unsigned long long *k0 = (unsigned long long *)buf, *k1 = (unsigned long long *)(buf + kb);
+    int *kbnd = (int *)(buf + 2 * kb + align256(tb));
+    int herr = 0;
+    const int kbl = (int)std::min<long long>((k + 255) / 256, (long long)sms * 8);
+    if (!e) e = cudaMemsetAsync(h->err, 0, sizeof(int), s);
+    if (!e) dyn_keys_kernel<<<kbl, 256, 0, s>>>(src, dst, k, (int)n, k0, h->err);
+    if (!e) e = cub::DeviceRadixSort::SortKeys(buf + 2 * kb, tb, k0, k1, k, 0, 64, s);
+    if (!e) dyn_ins_check_kernel<<<sms * 8, 256, 0, s>>>(h->a, h->ci, k1, k, h->err);
+    if (!e) e = cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e || herr) {
+        cudaFreeAsync(buf, s);
+        cudaStreamSynchronize(s);
+        return e ? e : cudaErrorInvalidValue;
+    }
+    // --- R: band-restricted BFS from the in-band endpoints
+    int hb[2] = {INT_MAX, INT_MIN};
+    if (!e) e = cudaMemcpyAsync(kbnd, hb, sizeof(hb), cudaMemcpyHostToDevice, s);
+    if (!e) dyn_ins_band_kernel<<<kbl, 256, 0, s>>>(k1, k, h->core, kbnd);
+    if (!e) e = cudaMemcpyAsync(hb, kbnd, sizeof(hb), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    const int kmin = hb[0];
+    const int kmax = (int)std::min<long long>((long long)hb[1] + k - 1, INT_MAX);
+    const long long nwords = (n + 31) / 32;
+    const long long arcs_old = h->arcs;
+    char *tmp = nullptr;
+    // vis | F0 | F1 | counters | deg (n+1) | est
+    const size_t tv = align256(sizeof(unsigned) * (size_t)std::max(nwords, 1ll));
+    const size_t tf = align256(sizeof(int) * (size_t)std::max(n, 1ll));
+    const size_t td = align256(sizeof(long long) * (size_t)(n + 1));
+    if (!e) e = lib_malloc_async(&tmp, tv + 3 * tf + 256 + td, s);
+    if (e) { cudaFreeAsync(buf, s); return e; }
+    unsigned *vis = (unsigned *)tmp;
+    int *F0 = (int *)(tmp + tv), *F1 = (int *)(tmp + tv + tf), *est = (int *)(tmp + tv + 2 * tf);
+    unsigned long long *cnt = (unsigned long long *)(tmp + tv + 3 * tf);
+    long long *deg = (long long *)(tmp + tv + 3 * tf + 256);
+    e = cudaMemsetAsync(vis, 0, tv, s);
+    if (!e) e = cudaMemsetAsync(cnt, 0, 256, s);
+    if (!e) dyn_ins_seed_kernel<<<kbl, 256, 0, s>>>(k1, k, h->core, kmin, kmax, vis, F0, cnt);
+    long long rsize = 0, bfs_levels = 0;
+    for (int par = 0; !e; par ^= 1) {
+        unsigned long long nf = 0;
+        e = cudaMemcpyAsync(&nf, cnt + par, sizeof(nf), cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e || nf == 0) break;
+        rsize += (long long)nf;
+        bfs_levels++;
+        if (!e) e = cudaMemsetAsync(cnt + (par ^ 1), 0, sizeof(unsigned long long), s);
+        const int bl = (int)std::min<long long>(((long long)nf * 32 + 255) / 256, (long long)sms * 16);
+        if (!e)
+            dyn_ins_bfs_kernel<<<std::max(bl, 1), 256, 0, s>>>(h->rp, h->ci, h->core, kmin, kmax, vis, par ? F1 : F0,
+                                                                (long long)nf, par ? F0 : F1, cnt + (par ^ 1));
+    }
+    // --- the new CSR: live arcs + both arcs of each new edge, sorted by (row, col)
+    const long long nkeys = arcs_old + 2 * k;
+    size_t tb2 = 0;
+    cub::DeviceRadixSort::SortKeys((void *)nullptr, tb2, (const unsigned long long *)nullptr,
+                                   (unsigned long long *)nullptr, nkeys);
+    size_t tbs = 0;
+    cub::DeviceScan::ExclusiveSum((void *)nullptr, tbs, (const long long *)nullptr, (long long *)nullptr, (int)(n + 1));
+    char *kbuf = nullptr;
+    const size_t kk = align256(sizeof(unsigned long long) * (size_t)nkeys);
+    if (!e) e = lib_malloc_async(&kbuf, 2 * kk + align256(std::max(tb2, tbs)), s);
+    if (e) { cudaFreeAsync(buf, s); cudaFreeAsync(tmp, s); return e; }
+    unsigned long long *a0 = (unsigned long long *)kbuf, *a1 = (unsigned long long *)(kbuf + kk);
+    if (!e) e = cudaMemsetAsync(deg + n, 0, sizeof(long long), s);
+    if (!e) dyn_ins_deg_kernel<<<sms * 8, 256, 0, s>>>(h->rp, h->ci, n, deg);
+    if (!e) dyn_ins_keys_kernel<<<sms * 8, 256, 0, s>>>(h->rp, h->ci, n, arcs_old, k1, k, deg, a0);
+    if (!e) e = cub::DeviceRadixSort::SortKeys(kbuf + 2 * kk, tb2, a0, a1, nkeys, 0, 64, s);
+    long long *rp_new = (long long *)a0;  // a0 is free after the sort: deg -> rowptr
+    if (!e) e = cub::DeviceScan::ExclusiveSum(kbuf + 2 * kk, tbs, deg, rp_new, (int)(n + 1), s);
+    long long arcs_new = 0;
+    if (!e) e = cudaMemcpyAsync(&arcs_new, rp_new + n, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (!e) dyn_ins_est_kernel<<<sms * 8, 256, 0, s>>>(h->core, vis, rp_new, n, k, est);
+    // --- a new handle state around the new CSR, HistoCore warm-started from est
+    void *ws_new = nullptr;
+    if (!e) e = lib_malloc_async(&ws_new, dyn_workspace_bytes(n, arcs_new, h->flags), s);
+    if (!e) {
+        char *p = (char *)ws_new + align256(hc_workspace_bytes(n, arcs_new, h->flags));
+        long long *rp2 = (long long *)p; p += align256(sizeof(long long) * (size_t)(n + 1));
+        int *ci2 = (int *)p; p += align256(sizeof(int) * (size_t)std::max(arcs_new, 1ll));
+        int *core2 = (int *)p; p += align256(sizeof(int) * (size_t)std::max(n, 1ll));
+        int *err2 = (int *)p;
+        e = cudaMemcpyAsync(rp2, rp_new, sizeof(long long) * (size_t)(n + 1), cudaMemcpyDeviceToDevice, s);
+        if (!e && arcs_new) dyn_ins_cols_kernel<<<sms * 8, 256, 0, s>>>(a1, arcs_new, ci2);
+        HcArgs a2;
+        if (!e) e = hc_run_t<false>(rp2, ci2, n, arcs_new, core2, s, h->flags, ws_new, st, h->dev, &a2, est);
+        if (!e) {
+            cudaFreeAsync(h->ws, s);
+            h->ws = ws_new;
+            h->rp = rp2;
+            h->ci = ci2;
+            h->core = core2;
+            h->err = err2;
+            h->arcs = arcs_new;
+            h->a = a2;
+            h->a.h0 = nullptr;  // est is freed below
+            ws_new = nullptr;
+        }
+    }
+    if (ws_new) cudaFreeAsync(ws_new, s);
+    cudaFreeAsync(kbuf, s);
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(buf, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (!e) e = e2;
+    if (!e && st) {
+        st->affected = rsize;  // |R|: vertices whose estimate was raised
+        st->bfs_levels = bfs_levels;
+    }
+    return e;
 }
 
 cudaError_t dyn_destroy(Dyn *h) {

@@ -92,6 +92,7 @@ cudaError_t dyn_create(const long long *rp, const int *ci, long long n, long lon
                        cudaStream_t s, const DevInfo &dev, pico_stats_t *st, Dyn **out);
 cudaError_t dyn_core(Dyn *h, int *core_out);
 cudaError_t dyn_delete(Dyn *h, const int *src, const int *dst, long long k, pico_stats_t *st);
+cudaError_t dyn_insert(Dyn *h, const int *src, const int *dst, long long k, pico_stats_t *st);
 cudaError_t dyn_destroy(Dyn *h);
 
 size_t validate_workspace_bytes();

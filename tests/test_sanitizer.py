@@ -1,7 +1,7 @@
 """compute-sanitizer memcheck / racecheck / synccheck over every
 kernel family of libpico on small graphs (HistoCore push / pull / host loop /
 debug check, PeelOne, CntCore, NbrCore, the sharded HistoCore and PeelOne kernels in loopback,
-the decremental update)."""
+the decremental update and an insertion)."""
 import os
 import re
 import shutil
@@ -31,6 +31,7 @@ if %r:
     src = torch.repeat_interleave(torch.arange(rp.numel() - 1, device=rp.device), rp[1:] - rp[:-1])
     m = src < ci
     d.delete_edges(src[m][:50].int(), ci[m][:50])
+    d.insert_edges(src[m][:50].int(), ci[m][:50])  # the same edges back: insertion path
     d.coreness()
     d.close()
 torch.cuda.synchronize()
