@@ -21,4 +21,6 @@ from .coreness import (  # noqa: F401
     brute_coreness,
     hindex_sorted,
     histogram_state,
+    brute_c,
+    exhaustive_mismatches,
 )

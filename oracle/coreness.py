@@ -44,6 +44,10 @@ def _load():
         lib.oracle_peel_levels.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P, _I64P, _I64P]
         lib.oracle_peel_levels.restype = ctypes.c_int64
         lib.oracle_kcore_check.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P]
+        lib.oracle_brute.argtypes = [ctypes.c_int64, ctypes.c_void_p, _I32P]
+        lib.oracle_brute.restype = ctypes.c_int
+        lib.oracle_exhaustive.argtypes = [ctypes.c_int64]
+        lib.oracle_exhaustive.restype = ctypes.c_int64
         lib.oracle_kcore_check.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -168,3 +172,22 @@ def histogram_state(rowptr, colidx, core, v: int) -> dict:
     out = {j: int(np.sum(nb == j)) for j in range(1, cv)}
     out[cv] = int(np.sum(nb >= cv))
     return out
+
+
+def brute_c(n: int, edges) -> list:
+    """oracle_brute (C): repeated minimum-degree removal on an adjacency matrix."""
+    lib = _load()
+    adj = np.zeros((n, n), dtype=np.uint8)
+    for u, v in edges:
+        if u != v:
+            adj[u, v] = adj[v, u] = 1
+    out = np.zeros(max(n, 1), dtype=np.int32)
+    if lib.oracle_brute(n, adj.ctypes.data, out.ctypes.data_as(_I32P)) != 0:
+        raise ValueError("oracle_brute: n must be <= 64")
+    return out[:n].tolist()
+
+
+def exhaustive_mismatches(n: int) -> int:
+    """Graphs on n vertices (all 2^(n(n-1)/2) of them) where BZ and the C brute
+    force differ."""
+    return int(_load().oracle_exhaustive(n))

@@ -33,6 +33,14 @@
  *                         G1: 2 levels / 3 sub-rounds.
  *   oracle_kcore_check    the definition itself: for every k the
  *                         subgraph induced by {core>=k} has min degree >= k.
+ *   oracle_brute          repeated removal of a minimum-degree vertex (Peel,
+ *                         Alg 1), O(n^2), its own adjacency
+ *                         matrix: the pin for BZ on tiny graphs.  Pinned
+ *                         against the pure-Python brute force of
+ *                         oracle/coreness.py on random graphs.
+ *   oracle_exhaustive     every labelled simple graph on n vertices (n <= 7:
+ *                         2^21 graphs) through oracle_bz and oracle_brute;
+ *                         returns the number of graphs where they differ.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -253,4 +261,68 @@ ORACLE_API int oracle_kcore_check(const int64_t *rowptr, const int32_t *colidx,
         if (core[v] < 0 || core[v] > rowptr[v + 1] - rowptr[v]) return 0;
     }
     return 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Brute force on an adjacency matrix (n <= 64): remove a
+ * vertex of minimum current degree (lowest id on ties); its coreness is the
+ * running maximum of the degrees at removal.  Independent of oracle_bz: no
+ * bins, no CSR traversal order.                                            */
+ORACLE_API int oracle_brute(int64_t n, const uint8_t *adj /* n*n, symmetric */, int32_t *core_out)
+{
+    if (n < 0 || n > 64) return -1;
+    int64_t deg[64];
+    char alive[64];
+    for (int64_t v = 0; v < n; v++) {
+        deg[v] = 0;
+        for (int64_t u = 0; u < n; u++) deg[v] += (u != v) && adj[v * n + u];
+        alive[v] = 1;
+    }
+    int64_t k = 0;
+    for (int64_t it = 0; it < n; it++) {
+        int64_t best = -1;
+        for (int64_t v = 0; v < n; v++)
+            if (alive[v] && (best < 0 || deg[v] < deg[best])) best = v;
+        if (deg[best] > k) k = deg[best];
+        core_out[best] = (int32_t)k;
+        alive[best] = 0;
+        for (int64_t u = 0; u < n; u++)
+            if (alive[u] && u != best && adj[best * n + u]) deg[u]--;
+    }
+    return 0;
+}
+
+/* Every labelled simple graph on n vertices (edge subsets in mask order):
+ * the CSR goes to oracle_bz, the adjacency matrix to oracle_brute.  Returns
+ * the number of graphs whose coreness vectors differ (-1: bad n).         */
+ORACLE_API int64_t oracle_exhaustive(int64_t n)
+{
+    if (n < 1 || n > 7) return -1;
+    int64_t np = n * (n - 1) / 2;
+    int32_t pu[21], pv[21];
+    int64_t q = 0;
+    for (int32_t i = 0; i < n; i++)
+        for (int32_t j = i + 1; j < n; j++) { pu[q] = i; pv[q] = j; q++; }
+    uint8_t adj[49];
+    int64_t rowptr[8];
+    int32_t colidx[42], cb[7], cr[7], fill[7];
+    int64_t bad = 0;
+    for (int64_t mask = 0; mask < ((int64_t)1 << np); mask++) {
+        memset(adj, 0, sizeof(adj));
+        for (int64_t e = 0; e < np; e++)
+            if (mask >> e & 1) { adj[pu[e] * n + pv[e]] = 1; adj[pv[e] * n + pu[e]] = 1; }
+        rowptr[0] = 0;
+        for (int64_t v = 0; v < n; v++) {
+            int64_t d = 0;
+            for (int64_t u = 0; u < n; u++) d += adj[v * n + u];
+            rowptr[v + 1] = rowptr[v] + d;
+            fill[v] = 0;
+        }
+        for (int64_t v = 0; v < n; v++)       /* rows ascending */
+            for (int64_t u = 0; u < n; u++)
+                if (adj[v * n + u]) colidx[rowptr[v] + fill[v]++] = (int32_t)u;
+        if (oracle_bz(rowptr, colidx, n, cb) != 0 || oracle_brute(n, adj, cr) != 0) return -1;
+        if (memcmp(cb, cr, sizeof(int32_t) * (size_t)n) != 0) bad++;
+    }
+    return bad;
 }

@@ -40,9 +40,9 @@
 //   the cap bin is only ever decremented).
 //   Two bit-exact directions apply the SAME (v, u) bin moves:
 //     push: changed rows are scanned, the moves hit u's histogram remotely;
-//     pull (dense rounds): every row u with core[u] > min core_t(C_t) is
-//       streamed, v is tested against the changed bitmap, the moves hit u's
-//       own histogram region (L2-local atomics).
+//     pull (dense rounds): every arc (u, v) of the edge list, bucketed by
+//       v-range, is streamed; v's record tells whether v changed, the moves
+//       hit u's own histogram (consecutive arcs share u: coalesced REDs).
 // SumHisto: walk k = core_old, core_old-1, ...; sum += histo[v][k];
 //   stop at the first k with sum >= k; core[v] = k,
 //   oldcore[v] = core_old, histo[v][k] = sum.

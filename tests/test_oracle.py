@@ -122,6 +122,49 @@ def test_exhaustive_n_le_6(oracle_mod):
                 assert list(oracle_mod.peel_levels(rp, ci)[0]) == b
 
 
+def test_exhaustive_n_le_7_in_c(oracle_mod):
+    """Every labelled simple graph on n <= 7 vertices (2^21 at n = 7): BZ ==
+    the C brute force (oracle_brute, its own adjacency matrix, SURVEY 8(c)
+    "brute force n <= 7 exhaustive")."""
+    for n in range(1, 8):
+        assert oracle_mod.exhaustive_mismatches(n) == 0, n
+
+
+def test_brute_c_matches_python_brute(oracle_mod):
+    """The C brute force is pinned to the pure-Python one on random
+    graphs up to n = 40, so the exhaustive check above rests on it."""
+    rng = random.Random(41)
+    for _ in range(300):
+        n = rng.randint(1, 40)
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        p = rng.random() * 0.6
+        e = [q for q in pairs if rng.random() < p]
+        assert oracle_mod.brute_c(n, e) == oracle_mod.brute_coreness(n, e), (n, e)
+
+
+def test_peel_subrounds_closed_forms(oracle_mod):
+    """Level and BSP sub-round counts of the level-synchronous peel on graphs
+    whose peel is known by hand: a path P_n peels one vertex from each end
+    per sub-round (1 level, ceil(n/2) sub-rounds); a cycle and K_n go in one
+    sub-round of one level; a star takes its leaves, then its centre (1
+    level, 2 sub-rounds); disjoint unions add their levels' sub-rounds."""
+    def run(n, e):
+        rp, ci = csr_np(n, e)
+        core, km, lv, sr = oracle_mod.peel_levels(rp, ci)
+        assert list(core) == oracle_mod.brute_coreness(n, e)
+        return lv, sr
+    for n in range(2, 13):
+        assert run(n, [(i, i + 1) for i in range(n - 1)]) == (1, (n + 1) // 2), n
+    for n in range(3, 10):
+        assert run(n, [(i, (i + 1) % n) for i in range(n)]) == (1, 1)
+        assert run(n, [(i, j) for i in range(n) for j in range(i + 1, n)]) == (1, 1)
+    for leaves in range(2, 9):
+        assert run(leaves + 1, [(0, i) for i in range(1, leaves + 1)]) == (1, 2)
+    # P5 + K4 (vertices 5..8): level 1 three sub-rounds, level 3 one
+    e = [(i, i + 1) for i in range(4)] + [(5 + i, 5 + j) for i in range(4) for j in range(i + 1, 4)]
+    assert run(9, e) == (2, 4)
+
+
 def test_random_n7(oracle_mod):
     rng = random.Random(7)
     pairs = [(i, j) for i in range(7) for j in range(i + 1, 7)]
