@@ -281,7 +281,8 @@ struct Tune {
     int b_max;      // class B (warp per vertex):   a_max < deg <= b_max
     int c_bins;     // class C (CTA per vertex) shared-memory bin cap
     int seg;        // arcs per UpdateHisto segment
-    int pull_div;   // pull-mode UpdateHisto when arcs(C_t) >= 2m / pull_div
+    int pull_div;   // sharded: pull-mode UpdateHisto when arcs(C_t) >= 2m / pull_div
+    int pull_tenths;  // one GPU: pull when 10 arcs(C_t) >= pull_tenths 2m
 };
 
 }  // namespace pico

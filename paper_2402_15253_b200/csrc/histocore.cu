@@ -143,7 +143,15 @@ struct HcArgs {
     // min(h0[u], h0[v]); null = the degrees
     const int *h0;
     int *psrc, *pdst;
+    // 32-bit copy of rowptr when 2m < 2^32 (null otherwise): the histogram-base
+    // gathers of UpdateHisto / SumHisto read half the bytes
+    unsigned *rp32;
 };
+
+// rowptr[v] through the 32-bit copy when there is one (uniform branch)
+__device__ __forceinline__ long long rp_at(const HcArgs &a, long long v) {
+    return a.rp32 ? (long long)__ldg(a.rp32 + v) : __ldg(a.rp + v);
+}
 
 // prefix of v's bucket-ordered row that UpdateHisto must scan after v's
 // estimate became c: entries with bucket >= floor(log2(c + 1)) (binary
@@ -235,6 +243,10 @@ __global__ void hc_degree_kernel(HcArgs a) {
         int v = (int)(it * nthreads + blockIdx.x * blockDim.x + threadIdx.x);
         bool valid = v < a.n;
         long long d = valid ? a.rp[v + 1] - a.rp[v] : 0;
+        if (valid && a.rp32) {
+            a.rp32[v] = (unsigned)a.rp[v];
+            if (v == a.n - 1) a.rp32[a.n] = (unsigned)a.rp[a.n];
+        }
         if (valid) {
             a.oldc[v] = (int)d;  // round-0 estimate of every vertex
             a.core[v] = (int)d;
@@ -930,7 +942,7 @@ __device__ void update_phase(const HcArgs &a, int t) {
                 if (STATS) st_arcs += cur.v[q] >= 0;
                 bool g = cur.v[q] >= 0 && cu[q] > cvo[q];  // N1/N3 neighbour
                 if (STATS) st_guard += g;
-                hb[q] = g ? __ldg(a.rp + cur.v[q]) - 1 : LLONG_MIN;  // rowptr[0] - 1 = -1 is valid
+                hb[q] = g ? rp_at(a, cur.v[q]) - 1 : LLONG_MIN;  // rowptr[0] - 1 = -1 is valid
             }
 #pragma unroll
             for (int q = 0; q < UA; q++)
@@ -1095,7 +1107,7 @@ __device__ void coo_pull_phase(const HcArgs &a, int t, const typename VR::T *vre
         for (int q = 0; q < UA; q++) {
             ru[q] = u[q] >= 0 ? ld_rec(a.rec + u[q], hot) : 0u;
             rv[q] = u[q] >= 0 ? __ldcg(vrec + v[q]) : 0;
-            hb[q] = u[q] >= 0 ? __ldg(a.rp + u[q]) - 1 : 0;
+            hb[q] = u[q] >= 0 ? rp_at(a, u[q]) - 1 : 0;
         }
 #pragma unroll
         for (int q = 0; q < UA; q++) {
@@ -1147,8 +1159,8 @@ __device__ __forceinline__ void sum_lanes(const HcArgs &a, int t, bool valid, in
     bool done = true;
     if (valid) {
         cold = __ldcg(a.core + v);
-        hb = __ldg(a.rp + v) - 1;  // bin b at hb + b
-        d = __ldg(a.rp + v + 1) - hb - 1;
+        hb = rp_at(a, v) - 1;  // bin b at hb + b
+        d = rp_at(a, v + 1) - hb - 1;
         k = cold;
         done = false;
         // (a broken invariant can walk k below 1 here: the warp loop below
@@ -1267,7 +1279,7 @@ __device__ void collect_sum_phase(const HcArgs &a, int t) {
                 v = (int)(wi * 32 + (__ffs(w) - 1));
                 w &= w - 1;
                 int cu = __ldcg(a.core + v);
-                valid = __ldcg(a.histo + __ldg(a.rp + v) + cu - 1) < cu;  // cnt < core
+                valid = __ldcg(a.histo + rp_at(a, v) + cu - 1) < cu;  // cnt < core
             }
             sum_lanes<STATS>(a, t, valid, v, acc, st_bins, nS);
         }
@@ -1295,7 +1307,7 @@ __device__ __forceinline__ bool update_prologue(const HcArgs &a, int t, bool lea
     for (long long w = gthread; w < a.nwords; w += nthreads) clr[w] = 0u;
     unsigned long long ac = bcast_u64(&a.ctl->arcsC[t & 1]);
     if (leader && (unsigned long long)t < a.fsz_cap) a.rarcs[t] = ac;
-    return a.allow_pull && ac * (unsigned long long)a.tn.pull_div >= (unsigned long long)a.arcs;
+    return a.allow_pull && 10ull * ac >= (unsigned long long)a.tn.pull_tenths * (unsigned long long)a.arcs;
 }
 
 // ---------------------------------------------------------------------------
@@ -1374,8 +1386,15 @@ Tune hc_tune(uint32_t flags) {
 #ifndef PICO_PULL_DIV
 #define PICO_PULL_DIV 2
 #endif
-    t.pull_div = PICO_PULL_DIV;  // pull when sum_{v in C_t} deg(v) >= 2m / pull_div
-    if (flags & PICO_F_PULL_ALWAYS) t.pull_div = 1 << 30;
+#ifndef PICO_PULL_TENTHS
+#define PICO_PULL_TENTHS 4
+#endif
+    t.pull_div = PICO_PULL_DIV;  // shards: pull when sum_{v in C_t} deg(v) >= 2m / pull_div
+    // one GPU: pull when sum_{v in C_t} deg(v) >= 0.4 * 2m (RMAT-26 per-round
+    // A/B, profiles/r02/rounds_T_*: round 10 at 0.42 pulls in 10.4 ms against
+    // 11.5 ms of push, round 11 at 0.38 pushes in 8.3 ms against 10.1)
+    t.pull_tenths = PICO_PULL_TENTHS;
+    if (flags & PICO_F_PULL_ALWAYS) { t.pull_div = 1 << 30; t.pull_tenths = 0; }
     return t;
 }
 
@@ -1408,7 +1427,7 @@ static int hc_npass(long long n, uint32_t flags, int rb = 4) {
 }
 
 struct HcLayout {
-    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, e16, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
+    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, e16, rp32, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
         elc, elt, total;
     long long nwords, scap, hcap, nbcap;
     size_t eltb;
@@ -1436,6 +1455,7 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags, long long
     L.c16 = b; b += align256(sizeof(unsigned short) * (size_t)n);
     L.rec = b; b += align256(sizeof(unsigned) * (size_t)n);
     L.e16 = b; b += align256(sizeof(unsigned short) * (size_t)n);
+    L.rp32 = b; b += align256(sizeof(unsigned) * (size_t)(n + 1));
     L.oldc = b; b += align256(sizeof(int) * (size_t)n);
     L.F = b; b += align256(sizeof(int) * (size_t)n);
     L.BC = b; b += align256(sizeof(int) * (size_t)n);
@@ -1531,6 +1551,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.c16 = (unsigned short *)(p + L.c16);
     a.rec = (unsigned *)(p + L.rec);
     a.e16 = (unsigned short *)(p + L.e16);
+    a.rp32 = arcs < (1ll << 32) ? (unsigned *)(p + L.rp32) : nullptr;
     a.oldc = (int *)(p + L.oldc);
     a.F = (int *)(p + L.F);
     a.BC = (int *)(p + L.BC);
@@ -1685,7 +1706,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
                     return err;
                 if ((err = cudaStreamSynchronize(s))) return err;
                 harcs.push_back(ac);
-                int pull = a.allow_pull && ac * (unsigned long long)tn.pull_div >= (unsigned long long)arcs;
+                int pull = a.allow_pull && 10ull * ac >= (unsigned long long)tn.pull_tenths * (unsigned long long)arcs;
                 tm.start(PICO_K_UPDATE);
                 hc_update_kernel<STATS><<<blocks, 512, 0, s>>>(a, t, pull);
                 tm.stop();
@@ -2106,6 +2127,7 @@ cudaError_t shard_create(const long long *rp, const int *ci, long long nloc, lon
     if (L.npass == 1) a.pdst = const_cast<int *>(ci);
     a.prefilter = 0;  // the shard's push UpdateHisto walks the CSC, not the rows
     a.h0 = nullptr;
+    a.rp32 = nullptr;  // (the shard's kernels read the 64-bit local rowptr)
     p += align256(L.total);
     h->deg8g = (shadow_t *)p; p += align256(sizeof(shadow_t) * (size_t)ng);
     h->deg16g = (unsigned short *)p; p += align256(sizeof(unsigned short) * (size_t)ng);
