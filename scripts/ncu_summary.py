@@ -2,6 +2,7 @@
 """Summarise ncu captures of one bench step into profiles/.
 
     python scripts/ncu_summary.py CONFIG ALGO REPORT.ncu-rep|RAW.csv [--out profiles/ncu_traffic.json]
+    (ALGO is ignored: every kernel is keyed by the algorithm that launched it)
                                   [--md profiles/r01/ncu_CONFIG_ALGO.md]
 
 Maps kernels to bench.py's kernel slots (degree / init / rounds / peel /
@@ -54,17 +55,27 @@ def main():
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    # kernels are keyed by the algorithm whose call launched them: hc_* ->
+    # histocore, po_* -> peelone; the shared compaction (rl_*, scans) belongs
+    # to the call it runs in (scripts/one_call.py runs HistoCore first, then
+    # PeelOne), i.e. its first launch to histocore, its second to peelone
     agg, lines, seen = {}, [], set()
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
         name = d.get("Kernel Name", "")
-        # one step = one launch of each distinct kernel (the bench's STATS run
-        # and timed runs use different template instances of the same kernel)
         base = name.split("<")[0].split("(")[0].replace("void ", "").strip()
-        if base in seen:
+        if "hc_" in base:
+            kalgo = "histocore"
+        elif "po_" in base:
+            kalgo = "peelone"
+        else:
+            kalgo = "histocore" if (base, "histocore") not in seen else "peelone"
+        # one step = one launch of each distinct kernel per algorithm (the
+        # bench's STATS run and timed runs use different template instances)
+        if (base, kalgo) in seen:
             continue
-        seen.add(base)
+        seen.add((base, kalgo))
         slot = slot_of(name)
         vals = {}
         for mtr in METRICS:
@@ -75,10 +86,11 @@ def main():
             if v != v:  # nan (metric not collected for this launch)
                 continue
             vals[mtr] = v * SCALE.get(mtr, {}).get(u.get(mtr, ""), 1.0)
-        lines.append((name[:60], slot, vals))
+        lines.append((name[:60], f"{kalgo}/{slot}", vals))
         if slot is None:
             continue
-        a = agg.setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": [], "l2w": 0.0})
+        a = agg.setdefault(kalgo, {}).setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": [],
+                                                        "l2w": 0.0})
         a["dram_bytes_per_step"] += vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0)
         a["time_s"] += vals.get("gpu__time_duration.sum", 0)
         # time-weighted L2 throughput (% of peak) of the slot's kernels: the second ceiling
@@ -90,10 +102,11 @@ def main():
             allj = json.load(f)
     except Exception:
         allj = {}
-    allj.setdefault(cfg, {})[algo] = {k: {"dram_bytes_per_step": v["dram_bytes_per_step"],
-                                          "ncu_time_s": v["time_s"], "kernels": v["kernels"],
-                                          "l2_throughput_pct": v["l2w"] / v["time_s"] if v["time_s"] else None,
-                                          "source": rep} for k, v in agg.items()}
+    for kalgo, slots in agg.items():
+        allj.setdefault(cfg, {})[kalgo] = {k: {"dram_bytes_per_step": v["dram_bytes_per_step"],
+                                               "ncu_time_s": v["time_s"], "kernels": v["kernels"],
+                                               "l2_throughput_pct": v["l2w"] / v["time_s"] if v["time_s"] else None,
+                                               "source": rep} for k, v in slots.items()}
     with open(out, "w") as f:
         json.dump(allj, f, indent=1, sort_keys=True)
     if md:
@@ -110,7 +123,7 @@ def main():
                         f"{v.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
                         f"{v.get('lts__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
                         f"{v.get('launch__registers_per_thread', 0):.0f} |\n")
-    print(json.dumps(allj[cfg][algo], indent=1))
+    print(json.dumps(allj[cfg], indent=1))
 
 
 if __name__ == "__main__":
