@@ -122,7 +122,7 @@ enum {
     PICO_F_NO_RELABEL = 512u  /* never compact (default: compact when n >=   */
                               /* pico_relabel_threshold() and >= 10% of the  */
                               /* ids are isolated, so per-vertex arrays fit  */
-                              /* the L2)                                     */
+                              /* the L2; PeelOne compacts only when forced)  */
 };
 
 /* Vertex count above which pico_coreness_ex relabels internally by default. */

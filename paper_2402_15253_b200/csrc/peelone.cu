@@ -37,6 +37,9 @@
 #ifndef PICO_PO_KHI0
 #define PICO_PO_KHI0 32  // initial near window: vertices of degree <= 32
 #endif
+#ifndef PICO_PO_THREADS
+#define PICO_PO_THREADS 512  // threads per CTA of the persistent level kernel
+#endif
 #ifndef PICO_PO_PER
 #define PICO_PO_PER 3  // resident CTAs per SM of the persistent level kernel
 #endif
@@ -377,7 +380,7 @@ __global__ void po_init_kernel(PoArgs a) {
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(512, PICO_PO_PER) po_levels_kernel(PoArgs a) {
+__global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel(PoArgs a) {
     constexpr bool CLAMP_SUB = MODE == 1;
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
@@ -587,10 +590,10 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         }
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, po_levels_kernel<MODE, STATS>, 512, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, po_levels_kernel<MODE, STATS>, PICO_PO_THREADS, 0);
         int per = std::max(1, std::min(occ, PICO_PO_PER));
         void *args[] = {&a};
-        err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<MODE, STATS>, sms * per, 512,
+        err = cudaLaunchCooperativeKernel((const void *)po_levels_kernel<MODE, STATS>, sms * per, PICO_PO_THREADS,
                                           args, 0, s);
         if (err) return err;
         launches++;
