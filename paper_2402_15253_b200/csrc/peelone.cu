@@ -391,11 +391,22 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
     int khi = a.khi0, fp = 0;  // near window bound, far list parity (uniform)
     for (int L = 0;; L++) {
         const int p = L & 1;
-        long long na = (long long)bcast_u64(&c->nAlive[p]);
-        const long long nf = (long long)bcast_u64(&c->nFar[fp]);
+        // the level head's control words, loaded by one thread back to back
+        // and broadcast through shared memory (one round trip, one barrier pair)
+        __shared__ long long s_head[5];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const long long h0 = (long long)ld_volatile(&c->nAlive[p]), h1 = (long long)ld_volatile(&c->nFar[fp]);
+            const int h2 = ld_volatile(&c->kminb[p]), h3 = ld_volatile(&c->fmin[fp]);
+            const unsigned long long h4 = ld_volatile(&c->q_snap);
+            s_head[0] = h0; s_head[1] = h1; s_head[2] = h2; s_head[3] = h3; s_head[4] = (long long)h4;
+        }
+        __syncthreads();
+        long long na = s_head[0];
+        const long long nf = s_head[1];
         if (leader && L > 0) po_close_level(a, p ^ 1, kprev);
         if (na == 0 && nf == 0) break;
-        k = max(k + 1, min(bcast_i32(&c->kminb[p]), nf ? bcast_i32(&c->fmin[fp]) : INT_MAX));
+        k = max(k + 1, min((int)s_head[2], nf ? (int)s_head[3] : INT_MAX));
         unsigned long long ts0 = leader ? globaltimer() : 0, ts1 = 0, S0 = S;
         if (nf && (k > khi || na == 0)) {
             // uniform: the window is exhausted (or the near list empty): rebuild
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             const long long nf2 = (long long)bcast_u64(&c->nFar[fp]);
             k = max(k, min(bcast_i32(&c->kminb[p]), nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
         }
-        unsigned long long lstart = bcast_u64(&c->q_snap);
+        const unsigned long long lstart = (unsigned long long)s_head[4];  // (a rebuild leaves q_snap alone)
         po_scan_phase<STATS>(a, k, p, gthread, nthreads);
         grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
         if (leader) ts1 = globaltimer();
