@@ -538,8 +538,9 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="extra PICO_F_* flags (A/B runs)")
     ap.add_argument("--extras", default="C2,C3",
                     help="other single-GPU configs timed after the headline (comma list; '' for none)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
-                    help="sharded path: NCCL inside libpico (pico_coreness_sharded) or torch.distributed")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "lsa", "torch"],
+                    help="sharded path: NCCL inside libpico (pico_coreness_sharded), the same with the "
+                         "device-side exchange over NCCL's device API (PICO_F_LSA_EXCHANGE), or torch.distributed")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded path even at one rank (torchrun --nproc-per-node 1)")
     args = ap.parse_args()

@@ -97,10 +97,14 @@ def bench_sharded(args):
         bench.log(f"[bench-sharded] {args.config}: n={n} m={m} local arcs {ci_l.numel()} generated in {t_gen:.1f}s ({gen_note})")
 
     comm, exchange_note = None, "torch.distributed"
-    if args.exchange == "nccl":
+    if args.exchange in ("nccl", "lsa"):
         try:
             comm = sharded.NcclComm()
             exchange_note = "NCCL inside libpico (pico_coreness_sharded)"
+            if args.exchange == "lsa" and args.algo != "peelone":
+                args.flags |= pico.F_LSA_EXCHANGE
+                exchange_note = ("NCCL device API inside libpico (symmetric window, LSA peer loads, one LSA "
+                                 "barrier per round, no host synchronisation per round)")
         except Exception as e:  # no usable libnccl: the torch.distributed exchange (also GPU, also NCCL)
             exchange_note = f"torch.distributed (in-library NCCL unavailable: {e})"
 

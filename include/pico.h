@@ -119,10 +119,17 @@ enum {
     PICO_F_PULL_ALWAYS = 128u,/* HistoCore: pull direction in every round    */
     PICO_F_RELABEL = 256u,    /* force the internal compaction of isolated   */
                               /* vertex ids (result mapped back, bit-exact)  */
-    PICO_F_NO_RELABEL = 512u  /* never compact (default: compact when n >=   */
+    PICO_F_NO_RELABEL = 512u, /* never compact (default: compact when n >=   */
                               /* pico_relabel_threshold() and >= 10% of the  */
                               /* ids are isolated, so per-vertex arrays fit  */
                               /* the L2; PeelOne compacts only when forced)  */
+    PICO_F_LSA_EXCHANGE = 32768u /* pico_coreness_sharded_ex, HistoCore: the */
+                              /* per-round exchange on the device through    */
+                              /* NCCL's device API (symmetric window, LSA    */
+                              /* peer loads, one LSA barrier per round), no  */
+                              /* host synchronisation per round; needs NCCL  */
+                              /* >= 2.28 and one NVLink domain, else         */
+                              /* PICO_ENOTSUP (include/pico_shard.h)         */
 };
 
 /* Vertex count above which pico_coreness_ex relabels internally by default. */

@@ -163,7 +163,17 @@ int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const i
 /* Same with PICO_F_* schedule flags and optional stats, identical on every
  * rank.  HistoCore: rounds = l2 and, when stats->frontier_sizes is set, the
  * GLOBAL |C_t| per round.  PeelOne: levels, subrounds, kmax and, in
- * frontier_sizes, the vertices processed per non-empty level (global). */
+ * frontier_sizes, the vertices processed per non-empty level (global).
+ * PICO_F_LSA_EXCHANGE (HistoCore): the round's exchange runs on the device
+ * over NCCL's device API -- each rank's pack kernel writes its triples into
+ * a symmetric window (ncclMemAlloc + ncclCommWindowRegister, identical size
+ * on every rank), a one-warp kernel stores its count into every peer's count
+ * row and passes one LSA barrier (release/acquire), and a copy kernel loads
+ * the peers' triples over NVLink in rank order; the host enqueues rounds in
+ * batches (PICO_LSA_BATCH, default 4) and reads the global counts once per
+ * batch (rounds after convergence are empty no-ops).  Same coreness, l2 and
+ * |C_t| as the host exchange.  PICO_ENOTSUP (nothing computed) when the
+ * loaded NCCL lacks the device API or the ranks are not one LSA team. */
 int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
                              int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,
                              int32_t *core_out_local, pico_stream_t stream, uint32_t flags,

@@ -15,12 +15,12 @@ import ctypes
 
 import numpy as np
 
-from ._lib import (ALGOS, F_DEBUG_INVARIANTS, F_L2_PERSIST, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY,  # noqa: F401
+from ._lib import (ALGOS, F_DEBUG_INVARIANTS, F_L2_PERSIST, F_PREFILTER, F_CLAMP_CAS, F_CLAMP_SUB, F_HOST_LOOP, F_NO_RELABEL, F_PULL_ALWAYS, F_PUSH_ONLY, F_LSA_EXCHANGE,  # noqa: F401
                    F_RELABEL, F_STATS, F_TIMING, F_TINY_TILES, F_VALIDATE, PicoError, Stats, check, header_functions, load)
 
 __all__ = ["coreness", "coreness_host", "clamp_hammer", "workspace_bytes", "DynamicCoreness", "PicoError", "Stats", "load",
            "F_VALIDATE", "F_STATS", "F_TIMING", "F_HOST_LOOP", "F_CLAMP_SUB", "F_TINY_TILES",
-           "F_PUSH_ONLY", "F_PULL_ALWAYS", "F_RELABEL", "F_NO_RELABEL", "F_CLAMP_CAS", "F_PREFILTER", "F_L2_PERSIST"]
+           "F_PUSH_ONLY", "F_PULL_ALWAYS", "F_RELABEL", "F_NO_RELABEL", "F_CLAMP_CAS", "F_PREFILTER", "F_L2_PERSIST", "F_LSA_EXCHANGE"]
 
 
 def _algo(algo) -> int:

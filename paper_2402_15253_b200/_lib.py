@@ -26,6 +26,7 @@ F_CLAMP_CAS = 1024
 F_PREFILTER = 2048
 F_DEBUG_INVARIANTS = 4096
 F_L2_PERSIST = 16384
+F_LSA_EXCHANGE = 32768
 
 K_NAMES = ["degree", "init", "rounds", "sum", "update", "peel", "validate", "relabel", "edgelist"]
 

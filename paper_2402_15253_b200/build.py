@@ -26,6 +26,25 @@ LINK_FLAGS = [
 ]
 
 
+def nccl_device_include() -> str | None:
+    """Include directory of an NCCL >= 2.28 with the device API headers
+    (nccl_device.h), e.g. the nvidia-nccl wheel torch depends on; None if
+    absent (lsa_exchange.cu then builds its stub)."""
+    cands = [os.environ.get("PICO_NCCL_INCLUDE")]
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec and spec.submodule_search_locations:
+            cands += [os.path.join(p, "include") for p in spec.submodule_search_locations]
+    except (ImportError, ValueError):
+        pass
+    cands += glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia", "nccl", "include"))
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "nccl_device.h")):
+            return c
+    return None
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -61,7 +80,11 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     with tempfile.TemporaryDirectory(prefix="pico_build_") as d:
         def compile_one(src):
             obj = os.path.join(d, os.path.basename(src) + ".o")
-            cmd = ([nvcc()] + NVCC_FLAGS + ["-D" + x for x in defines]
+            extra = []
+            if os.path.basename(src) == "lsa_exchange.cu":
+                inc = nccl_device_include()
+                extra = ["-I" + inc, "-DPICO_HAVE_NCCL_DEVICE=1"] if inc else ["-DPICO_HAVE_NCCL_DEVICE=0"]
+            cmd = ([nvcc()] + NVCC_FLAGS + ["-D" + x for x in defines] + extra
                    + ["-I" + INCLUDE, "-I" + CSRC, "-c", src, "-o", obj])
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)

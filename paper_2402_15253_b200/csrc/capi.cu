@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "lsa_exchange.h"
 #include "pico_shard.h"
 #include "pico_dyn.h"
 
@@ -658,6 +659,12 @@ NcclApi &nccl() {
 struct pico_comm_s {
     ncclComm_t c;
     int nranks, rank;
+    // device-side exchange state (PICO_F_LSA_EXCHANGE): the symmetric window
+    // and device communicator, created at the first such call and kept for
+    // the communicator's lifetime (registration is collective and costly);
+    // recreated -- on every rank alike -- when a call needs a larger capacity
+    pico::LsaX *lsa = nullptr;
+    long long lsa_cap = 0;
 };
 
 static int nccl_fail(ncclResult_t r, const char *where) {
@@ -782,9 +789,76 @@ int pico_comm_size(pico_comm_t comm, int *nranks, int *rank) {
 int pico_comm_destroy(pico_comm_t comm) {
     g_last_error.clear();
     if (!comm) return PICO_OK;
+    if (comm->lsa) pico::lsa_destroy(comm->lsa);  // before the communicator it was registered with
     ncclResult_t r = nccl().CommDestroy(comm->c);
     delete comm;
     return r == ncclSuccess ? PICO_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+// HistoCore rounds with the device-side exchange (PICO_F_LSA_EXCHANGE,
+// lsa_exchange.cu): pack into this rank's half of the symmetric window, LSA
+// counts + barrier + peer copies, apply with the device total; rounds are
+// enqueued PICO_LSA_BATCH at a time and the host reads the batch's global
+// counts once (the first empty round is the convergence; later rounds of the
+// batch are no-ops on every rank, so the barriers stay matched).
+static int lsa_rounds(pico_comm_t comm, Shard *sh, const std::vector<long long> &hm, long long n_global,
+                      long long arcs_global, pico_stats_t *stats, cudaStream_t s, const DevInfo &dev) {
+    const int P = comm->nranks, me = comm->rank;
+    long long cap = 1;
+    for (int r = 0; r < P; r++) cap = std::max(cap, hm[3 * r + 1] - hm[3 * r]);
+    std::string msg;
+    cudaError_t e = cudaSuccess;
+    if (!comm->lsa || comm->lsa_cap < cap) {  // the same decision on every rank (cap is global)
+        if (comm->lsa) {
+            if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "LSA exchange setup");
+            lsa_destroy(comm->lsa);
+            comm->lsa = nullptr;
+        }
+        e = lsa_create((void *)comm->c, P, me, cap, &comm->lsa, &msg);
+        if (e == cudaErrorNotSupported) return fail(PICO_ENOTSUP, "LSA exchange unavailable: %s", msg.c_str());
+        if (e) return msg.empty() ? cuda_fail(e, "LSA exchange setup") : fail(PICO_ENCCL, "%s", msg.c_str());
+        comm->lsa_cap = cap;
+    }
+    LsaX *lx = comm->lsa;
+    int batch = 4;
+    if (const char *b = getenv("PICO_LSA_BATCH")) batch = std::max(1, std::min(64, atoi(b)));
+    int *all = nullptr;
+    long long *tot = nullptr;
+    int rc = PICO_OK;
+    std::vector<long long> htot(batch);
+    do {
+        if ((e = lib_malloc_async(&all, sizeof(int) * 3 * (size_t)std::max(n_global, 1ll), s)) ||
+            (e = lib_malloc_async(&tot, sizeof(long long) * (size_t)batch, s))) { rc = cuda_fail(e, "alloc"); break; }
+        long long rounds = 0;
+        bool done = false;
+        while (!done) {
+            for (int b = 0; b < batch && rc == PICO_OK; b++) {
+                const int par = (int)((rounds + b) & 1);
+                const unsigned long long *cdev = nullptr;
+                if ((e = shard_pack_dev(sh, lsa_send_buffer(lx, par), &cdev)) ||
+                    (e = lsa_exchange(lx, par, cdev, all, tot + b, dev.sms * 8, s)) ||
+                    (e = shard_apply(sh, all, 0, nullptr, lsa_total(lx))))
+                    rc = cuda_fail(e, "LSA round");
+            }
+            if (rc != PICO_OK) break;
+            if ((e = cudaMemcpyAsync(htot.data(), tot, sizeof(long long) * (size_t)batch, cudaMemcpyDeviceToHost, s)) ||
+                (e = cudaStreamSynchronize(s))) { rc = cuda_fail(e, "LSA counts"); break; }
+            for (int b = 0; b < batch; b++) {
+                if (htot[b] == 0) { done = true; break; }
+                if (stats && stats->frontier_sizes && rounds < stats->frontier_sizes_cap)
+                    stats->frontier_sizes[rounds] = htot[b];
+                rounds++;
+            }
+            // every valid round lowers the sum of the estimates: l2 <= 2m (see the single-GPU guard)
+            if (!done && rounds > arcs_global + 2) { rc = fail(PICO_EGRAPH, "no convergence"); break; }
+        }
+        if (rc == PICO_OK && stats) stats->rounds = rounds;
+    } while (false);
+    if (all) cudaFreeAsync(all, s);
+    if (tot) cudaFreeAsync(tot, s);
+    cudaError_t es = cudaStreamSynchronize(s);
+    if (rc == PICO_OK && es) rc = cuda_fail(es, "LSA cleanup");
+    return rc;
 }
 
 int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
@@ -866,6 +940,12 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
         if (nr != ncclSuccess || ne != ncclSuccess) { bail_nccl(nr != ncclSuccess ? nr : ne, "allgatherv degrees"); break; }
         long long changed = 0;
         if ((e = shard_init(sh, deg_g, &changed))) { bail_cuda(e, "shard init"); break; }
+        if (flags & PICO_F_LSA_EXCHANGE) {
+            rc = lsa_rounds(comm, sh, hm, n_global, 2 * (long long)m_global, stats, s, dev);
+            if (rc != PICO_OK) break;
+            if (nloc > 0 && (e = shard_result(sh, core_out_local))) { bail_cuda(e, "shard result"); break; }
+            break;
+        }
         // rounds
         long long rounds = 0;
         for (;;) {

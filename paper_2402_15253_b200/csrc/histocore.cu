@@ -1899,8 +1899,11 @@ __global__ void sh_deg8_kernel(const int *deg, long long ng, shadow_t *d8, unsig
 
 // records of the received triples: (new, old) for the round's pull, then
 // (new, new) once the round is applied
+// total_dev (device exchange, lsa_exchange.cu): the triple count from device memory
 template <bool RESET>
-__global__ void sh_records_kernel(const int *tr, long long total, unsigned long long *grec) {
+__global__ void sh_records_kernel(const int *tr, long long total, unsigned long long *grec,
+                                  const unsigned long long *total_dev = nullptr) {
+    if (total_dev) total = (long long)*total_dev;
     long long nt = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += nt)
         grec[tr[3 * i]] = pack_rec64(tr[3 * i + 2], RESET ? tr[3 * i + 2] : tr[3 * i + 1]);
@@ -1954,7 +1957,9 @@ __global__ void sh_pack_kernel(HcArgs a, const unsigned long long *ns_dev, long 
 // (triple, segment) items for the CSC lists of the received triples; the
 // local arcs they touch are summed into *arcs_ct (the pull decision)
 __global__ void sh_segments_kernel(const int *tr, long long total, const long long *csc_off, int seg, int2 *TS,
-                                   unsigned long long *nTS, unsigned long long *arcs_ct) {
+                                   unsigned long long *nTS, unsigned long long *arcs_ct,
+                                   const unsigned long long *total_dev = nullptr) {
+    if (total_dev) total = (long long)*total_dev;
     long long nt = (long long)gridDim.x * blockDim.x;
     long long iters = (total + nt - 1) / nt;
     long long ac = 0;
@@ -2283,7 +2288,8 @@ cudaError_t shard_pack_dev(Shard *h, int *triples, const unsigned long long **co
 // rounds, pull over the bucketed local edge list against the global records
 // -- then SumHisto of the local frontier.  The direction is decided on the
 // device (sh_gate_kernel): no host round trip.
-cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed) {
+cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed,
+                        const unsigned long long *total_dev) {
     cudaStream_t s = h->s;
     HcArgs &a = h->a;
     const int sms = h->dev.sms;
@@ -2300,11 +2306,14 @@ cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh_pull_kernel, 512, 0);
     const int pblocks = sms * std::max(1, occ);
+    // device total (no host round trip): grids sized for any count, the
+    // kernels read it; an empty round is a no-op
+    if (total_dev) total = h->ng;
     if (total > 0) {
         int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-        if (h->pull_ok) sh_records_kernel<false><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec);
+        if (h->pull_ok) sh_records_kernel<false><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec, total_dev);
         sh_segments_kernel<<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->csc_off, a.tn.seg, h->TS, nTS,
-                                                               h->cnt + 2);
+                                                               h->cnt + 2, total_dev);
         sh_gate_kernel<<<1, 32, 0, s>>>(h->cnt, h->arcs, h->pull_ok ? 1 : 0, a.tn.pull_div);
         sh_update_kernel<<<sms * 2, 512, 0, s>>>(a, triples, h->TS, nTS, h->csc_off, h->csc_idx,
                                                  &a.ctl->nF[(t + 1) & 1], gate);
@@ -2314,7 +2323,7 @@ cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long
     if (h->pull_ok && total > 0) {
         sh_collect_kernel<<<pblocks, 512, 0, s>>>(a, t + 1, gate);
         int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-        sh_records_kernel<true><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec);
+        sh_records_kernel<true><<<std::max(blocks, 1), 256, 0, s>>>(triples, total, h->grec, total_dev);
     }
     if ((e = cudaGetLastError())) return e;
     h->t = t + 1;

@@ -68,7 +68,10 @@ cudaError_t shard_degrees(Shard *h, int *deg_out);
 cudaError_t shard_init(Shard *h, const int *deg_global, long long *changed);
 cudaError_t shard_pack(Shard *h, int *triples, long long cap, long long *count);
 cudaError_t shard_pack_dev(Shard *h, int *triples, const unsigned long long **count_dev);
-cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed);
+// total_dev (optional): the triple count in device memory (device-side
+// exchange); the host total is then ignored
+cudaError_t shard_apply(Shard *h, const int *triples, long long total, long long *changed,
+                        const unsigned long long *total_dev = nullptr);
 cudaError_t shard_result(Shard *h, int *core_out);
 cudaError_t shard_destroy(Shard *h);
 

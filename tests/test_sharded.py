@@ -423,3 +423,35 @@ def test_sharded_abi_single_rank_nccl():
             assert (run.levels, run.rounds, run.kmax) == (lv, sr, km)
     finally:
         comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", ["1", "3", "4"])
+def test_sharded_lsa_exchange_single_rank(batch, monkeypatch):
+    """PICO_F_LSA_EXCHANGE: the round's exchange on the device over NCCL's
+    device API (symmetric window, LSA barrier, peer loads), rounds enqueued in
+    batches with one host read per batch.  One rank: bit-exact coreness, l2
+    and every global |C_t| of the Jacobi reference, on R12 and C1, push,
+    pull-always and tiny-tile schedules, batch sizes that end the run at, before
+    and past a batch boundary."""
+    import torch
+    import oracle
+    import paper_2402_15253_b200 as pico
+    from paper_2402_15253_b200 import sharded
+    monkeypatch.setenv("PICO_LSA_BATCH", batch)
+    dev = torch.device("cuda:0")
+    comm = sharded.NcclComm(nranks=1, rank=0)
+    try:
+        for cfg in ("R12", "C1"):
+            rp_np, ci_np = synth.to_numpy(*synth.CONFIGS[cfg].build())
+            ref = oracle.bz(rp_np, ci_np)
+            _, l2, sizes = oracle.jacobi_rounds(rp_np, ci_np)
+            rp, ci = torch.from_numpy(rp_np).to(dev), torch.from_numpy(ci_np).to(dev)
+            n, m = rp.numel() - 1, ci.numel() // 2
+            for fl in (0, pico.F_TINY_TILES, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES):
+                run = sharded.coreness_sharded_nccl(rp, ci, n, m, 0, comm, flags=fl | pico.F_LSA_EXCHANGE)
+                torch.cuda.synchronize()
+                assert np.array_equal(run.core_local.cpu().numpy(), ref), (cfg, fl)
+                assert run.rounds == l2 and run.frontier_sizes == sizes, (cfg, fl, run.rounds, l2)
+    finally:
+        comm.close()
