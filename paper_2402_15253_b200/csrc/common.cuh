@@ -230,6 +230,9 @@ __device__ __forceinline__ void grid_barrier_snap(unsigned *arrive, unsigned *ge
 }
 
 // Workspace control block (device memory, initialised at the start of a call).
+#ifndef PICO_BAR_PAD
+#define PICO_BAR_PAD 0
+#endif
 struct Ctrl {
     // HistoCore lists: F (frontier vertex ids) and S (update segments),
     // double-buffered counts indexed by round parity (see histocore.cu).
@@ -249,7 +252,9 @@ struct Ctrl {
     alignas(128) unsigned long long q_tail;     // next queue slot to write
     alignas(128) unsigned long long q_pending;  // pushed, not fully processed
     alignas(128) unsigned long long q_snap;     // tail snapshot at the last barrier
-    unsigned long long nAlive[2];  // alive list lengths (ping-pong by level)
+    alignas(128) unsigned long long q_tail1;    // PeelOne: the queue's second append counter
+    alignas(128) unsigned long long nAlive[2];  // alive list lengths (ping-pong by level; own line: the
+                                                // scans append to these and to a queue counter at once)
     unsigned long long nFar[2];    // far list lengths (ping-pong by rebuild)
     int fmin[2];                   // min estimate in the far list (ping-pong)
     unsigned long long nProc[2];   // vertices processed per level (parity)
@@ -261,6 +266,10 @@ struct Ctrl {
     // grid barrier (own lines)
     alignas(128) unsigned bar_arrive;
     alignas(128) unsigned bar_gen;
+#if PICO_BAR_PAD
+    unsigned char bar_pad[PICO_BAR_PAD];  // A/B: the arrival word far from the hot counters
+#endif
+    alignas(128) unsigned bar_flip;  // grid_sync's arrival word
     // instrumentation (PICO_F_STATS)
     unsigned long long st_frontier;
     unsigned long long st_init_slots;
@@ -273,6 +282,45 @@ struct Ctrl {
     unsigned long long st_segs;
     unsigned long long st_pull;
 };
+
+// Grid barrier with one arrival word and no release word: CTA 0 adds
+// 2^31 - (nb - 1), every other CTA adds 1, so the word's top bit flips
+// exactly when the last CTA arrives, whatever the order, and the low bits
+// return to their value (the word starts at 0).  Every CTA polls the top bit
+// of the word it incremented.  scripts/micro/grid_barrier.cu: 1.23 us at 444
+// CTAs against 2.57 us for grid_barrier (whose last arriver resets the count
+// and bumps a separate generation word: one more serialised L2 round trip).
+// The PeelOne level kernel (~1,000 short phases at C2) uses it; HistoCore's
+// round kernel keeps grid_barrier, whose pollers back off: its phases last
+// milliseconds, and spinning CTAs cost its rounds ~0.5 % (profiles/r02/s3/).
+#ifndef PICO_BAR_SLEEP
+#define PICO_BAR_SLEEP 0  // ns of backoff per poll of the arrival word (A/B)
+#endif
+#ifndef PICO_BAR_GEN
+#define PICO_BAR_GEN 0  // A/B: grid_sync through the generation-word barrier
+#endif
+__device__ __forceinline__ void grid_sync(Ctrl *c) {
+#if PICO_BAR_GEN
+    grid_barrier(&c->bar_arrive, &c->bar_gen);
+    return;
+#endif
+    unsigned *bar = &c->bar_flip;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        const unsigned add = (blockIdx.x | blockIdx.y | blockIdx.z) == 0 ? 0x80000000u - (nb - 1) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(bar, add);
+        while (((old ^ *reinterpret_cast<volatile unsigned *>(bar)) & 0x80000000u) == 0) {
+#if PICO_BAR_SLEEP
+            __nanosleep(PICO_BAR_SLEEP);
+#endif
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 
 // Tunables (degree-class thresholds, bin caps).  PICO_F_TINY_TILES shrinks
 // them so all code paths are exercised by small test graphs.

@@ -57,7 +57,7 @@ struct PoArgs {
     int *far1;     // holds those with estimate <= khi, far[] the others
     int khi0;      // initial window bound (INT_MAX: no far list)
     unsigned *done;  // [n/32] processed bitmap: v entered a frontier (its coreness is final)
-    long long *Q;  // (v << 32) | segment
+    long long *Q;  // run-wide queue log: (v << 32) | segment
     unsigned long long *fsz;
     unsigned long long fsz_cap;
     unsigned long long *rtime;  // [2 fsz_cap] per scanned level: scan ns | k << 40, drain ns | sub-rounds << 40
@@ -67,9 +67,24 @@ struct PoArgs {
 
 __device__ __forceinline__ int po_nseg(long long d, int seg) { return (int)((d + seg - 1) / seg); }
 
-// Warp-cooperative append of vertices (pred lanes) to the queue tail, one entry
-// per `seg` arcs of the row.  Returns the number of vertices appended.
-__device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
+// The queue's append counters: a phase appends through counter y and reads
+// (after the barrier) the count of the other one, which no phase touches
+// meanwhile -- so every CTA reads the same frozen count without a snapshot.
+// Both counters are monotonic over the run; a phase's entries go to
+// Q[wbase + (counter - cbase)], wbase = the end of the entries it reads,
+// cbase = the counter's value when the phase started (see po_levels_kernel).
+__device__ __forceinline__ unsigned long long *po_cnt(const PoArgs &a, int y) {
+    return y ? &a.ctl->q_tail1 : &a.ctl->q_tail;
+}
+struct PoAppend {
+    unsigned long long wbase, cbase;
+    int y;
+};
+
+// Warp-cooperative append of vertices (pred lanes) to the queue (positions
+// from the phase's append counter, PoAppend), one entry per `seg` arcs of the
+// row.  Returns the number of vertices appended.
+__device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v, const PoAppend ap) {
     const int lane = lane_id();
     int ns = 0;
     if (pred) ns = po_nseg(__ldg(a.rp + v + 1) - __ldg(a.rp + v), a.seg);
@@ -86,7 +101,7 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return 0;
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.ctl->q_tail, (unsigned long long)total);
+    if (lane == 0) base = ap.wbase + (atomicAdd(po_cnt(a, ap.y), (unsigned long long)total) - ap.cbase);
     base = __shfl_sync(FULL, base, 0);
     // the warp writes the `total` entries jointly, so a hub's thousands of
     // entries do not serialise on its lane (one lane writing the 31K entries
@@ -109,9 +124,10 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v) {
     return __popc(__ballot_sync(FULL, pred));
 }
 
-// scan of level k (parity p): alive[p] -> frontier entries in Q, alive[p^1]
+// scan of level k (parity p): alive[p] -> frontier entries in the queue, alive[p^1]
 template <bool STATS>
-__device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, long long nthreads) {
+__device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, long long nthreads,
+                              const PoAppend ap) {
     const long long na = (long long)bcast_u64(&a.ctl->nAlive[p]);
     const int *alive = p ? a.alive1 : a.alive0;
     int *next = p ? a.alive0 : a.alive1;
@@ -130,7 +146,7 @@ __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, 
         bool keep = valid && c > k;  // c < k: already processed by an earlier level
         if (keep) kmin = min(kmin, c);
         warp_append(keep, v, next, &a.ctl->nAlive[p ^ 1]);
-        nproc += po_push(a, front, v);
+        nproc += po_push(a, front, v, ap);
     }
     kmin = warp_min(kmin);
     // po_push returns the warp-wide count to every lane: lane 0 holds the total
@@ -221,9 +237,11 @@ __device__ __forceinline__ int clamp_dec(int *p, int c, int k) {
 #ifndef PICO_PO_A
 #define PICO_PO_A 1  // arcs per lane per entry (entry = 32 * A arcs)
 #endif
+// reads queue entries [lo, hi), appends the next sub-round's through ap
 template <int MODE, bool STATS>
-__device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long lo, unsigned long long hi,
-                             int khi = INT_MAX, int *fminp = nullptr) {
+__device__ void po_sub_phase(const PoArgs &a, int k, int p, const PoAppend ap, unsigned long long lo,
+                             unsigned long long hi, int khi = INT_MAX, int *fminp = nullptr) {
+    const long long *Qx = a.Q;
     constexpr int U = PICO_PO_U, A = PICO_PO_A, W = U * A;
     const int lane = lane_id();
     const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -243,7 +261,7 @@ __device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long l
             long long b = 0;
             int len = 0;
             if (i < hi) {
-                long long e = __ldcg(a.Q + i);
+                long long e = __ldcg(Qx + i);
                 int v = (int)(e >> 32);
                 int s = (int)(e & 0xffffffffll);
                 long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
@@ -304,7 +322,7 @@ __device__ void po_sub_phase(const PoArgs &a, int k, int p, unsigned long long l
             if (__any_sync(FULL, cross[w])) warp_append(cross[w], u[w], p ? a.alive0 : a.alive1, &a.ctl->nAlive[p ^ 1]);
 #pragma unroll
         for (int w = 0; w < W; w++)
-            if (__any_sync(FULL, push[w])) nproc += po_push(a, push[w], u[w]);
+            if (__any_sync(FULL, push[w])) nproc += po_push(a, push[w], u[w], ap);
     }
     kmin = warp_min(kmin);
     fmin = warp_min(fmin);
@@ -379,6 +397,14 @@ __global__ void po_init_kernel(PoArgs a) {
 // ---------------------------------------------------------------------------
 // P1-P3: persistent cooperative kernel over all levels
 // ---------------------------------------------------------------------------
+// Queue positions without a snapshot: the scan of a level and every sub-round
+// append through one of two monotonic counters, alternating, so the counter
+// whose count the NEXT phase needs is frozen while it is read and every CTA
+// reads the same value straight from it after the barrier.  A phase writes
+// its entries right after the ones it reads (one run-wide log, as before).
+// Every barrier is then the plain grid_sync (one arrival word, no last-arriver
+// publication: 1.23 vs 2.57 us per barrier at 444 CTAs,
+// scripts/micro/grid_barrier.cu); the sub-rounds are unchanged.
 template <int MODE, bool STATS>
 __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel(PoArgs a) {
     constexpr bool CLAMP_SUB = MODE == 1;
@@ -387,19 +413,22 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     Ctrl *c = a.ctl;
     int k = 0, kprev = 0;
-    unsigned long long S = 0;  // global sub-round counter (claim counter parity)
+    unsigned long long S = 0;          // global sub-round counter
+    unsigned long long lo = 0;         // consumed prefix of the queue (uniform)
+    unsigned long long cb0 = 0, cb1 = 0;  // the counters' values at their last read (uniform; scalars, not
+                                          // a runtime-indexed array, which would live in local memory)
+    int y = 0;                         // the counter the next phase appends through (uniform)
     int khi = a.khi0, fp = 0;  // near window bound, far list parity (uniform)
     for (int L = 0;; L++) {
         const int p = L & 1;
         // the level head's control words, loaded by one thread back to back
         // and broadcast through shared memory (one round trip, one barrier pair)
-        __shared__ long long s_head[5];
+        __shared__ long long s_head[4];
         __syncthreads();
         if (threadIdx.x == 0) {
             const long long h0 = (long long)ld_volatile(&c->nAlive[p]), h1 = (long long)ld_volatile(&c->nFar[fp]);
             const int h2 = ld_volatile(&c->kminb[p]), h3 = ld_volatile(&c->fmin[fp]);
-            const unsigned long long h4 = ld_volatile(&c->q_snap);
-            s_head[0] = h0; s_head[1] = h1; s_head[2] = h2; s_head[3] = h3; s_head[4] = (long long)h4;
+            s_head[0] = h0; s_head[1] = h1; s_head[2] = h2; s_head[3] = h3;
         }
         __syncthreads();
         long long na = s_head[0];
@@ -413,7 +442,7 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             // the far list with a doubled window
             const int khi_new = (int)max((long long)khi, min(2ll * k + 16, (long long)INT_MAX - 1));
             po_rebuild_phase(a, khi, khi_new, fp, p, gthread, nthreads, STATS);
-            grid_barrier(&c->bar_arrive, &c->bar_gen);
+            grid_sync(c);
             if (leader) {
                 c->nFar[fp] = 0;  // consumed; refilled at the next rebuild
                 c->fmin[fp] = INT_MAX;
@@ -424,32 +453,37 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             const long long nf2 = (long long)bcast_u64(&c->nFar[fp]);
             k = max(k, min(bcast_i32(&c->kminb[p]), nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
         }
-        const unsigned long long lstart = (unsigned long long)s_head[4];  // (a rebuild leaves q_snap alone)
-        po_scan_phase<STATS>(a, k, p, gthread, nthreads);
-        grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
+        const unsigned long long lstart = lo;
+        po_scan_phase<STATS>(a, k, p, gthread, nthreads, PoAppend{lo, y ? cb1 : cb0, y});
+        grid_sync(c);
         if (leader) ts1 = globaltimer();
         if (leader) {
             c->nAlive[p] = 0;       // alive[p] consumed; refilled at level L+1
             c->kminb[p] = INT_MAX;  // consumed at this level's head
         }
-        unsigned long long lo = lstart;
         for (int sub = 0;; sub++) {
-            unsigned long long hi = bcast_u64(&c->q_snap);
-            if (hi == lo) {  // uniform: every CTA read the same snapshot
+            // entries appended by the previous phase through counter y: frozen,
+            // the phase about to run appends through y ^ 1
+            const unsigned long long cy = bcast_u64(po_cnt(a, y));
+            const unsigned long long hi = lo + (cy - (y ? cb1 : cb0));
+            if (y) cb1 = cy; else cb0 = cy;
+            y ^= 1;
+            if (hi == lo) {  // uniform: every CTA read the same frozen count
                 // an empty level has no sub-round barrier: one barrier orders
                 // the leader's resets above before the next level's scan
                 // appends to alive[p] / lowers kminb[p]
-                if (sub == 0) grid_barrier(&c->bar_arrive, &c->bar_gen);
+                if (sub == 0) grid_sync(c);
+                y ^= 1;  // nothing was appended through y: the next scan appends through it again
                 break;
             }
-            po_sub_phase<MODE, STATS>(a, k, p, lo, hi, khi, &c->fmin[fp]);
-            grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
+            po_sub_phase<MODE, STATS>(a, k, p, PoAppend{hi, y ? cb1 : cb0, y}, lo, hi, khi, &c->fmin[fp]);
+            grid_sync(c);
             lo = hi;
             S++;
         }
         if (CLAMP_SUB) {
             po_repair_phase(a, k, lstart, lo, gthread, nthreads);
-            grid_barrier_snap(&c->bar_arrive, &c->bar_gen, &c->q_tail, &c->q_snap);
+            grid_sync(c);
         }
         if (leader) {
             c->rounds = S;  // BSP sub-rounds so far
@@ -464,20 +498,20 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
 
 // host-loop variants (PICO_F_HOST_LOOP)
 template <bool STATS>
-__global__ void __launch_bounds__(512) po_scan_kernel(PoArgs a, int k, int p) {
+__global__ void __launch_bounds__(512) po_scan_kernel(PoArgs a, int k, int p, PoAppend ap) {
     const long long gthread = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * blockDim.x;
-    po_scan_phase<STATS>(a, k, p, gthread, nthreads);
+    po_scan_phase<STATS>(a, k, p, gthread, nthreads, ap);
 }
 
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(512) po_sub_kernel(PoArgs a, int k, int p, unsigned long long lo,
+__global__ void __launch_bounds__(512) po_sub_kernel(PoArgs a, int k, int p, PoAppend ap, unsigned long long lo,
                                                      unsigned long long hi, int first) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && first) {
         a.ctl->nAlive[p] = 0;
         a.ctl->kminb[p] = INT_MAX;
     }
-    po_sub_phase<MODE, STATS>(a, k, p, lo, hi);
+    po_sub_phase<MODE, STATS>(a, k, p, ap, lo, hi);
 }
 
 __global__ void po_repair_kernel(PoArgs a, int k, unsigned long long lo, unsigned long long hi) {
@@ -562,8 +596,8 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     tstart(PICO_K_PEEL);
     if (flags & PICO_F_HOST_LOOP) {
         int blocks = sms * 4;
-        int k = 0, kprev = 0;
-        unsigned long long tail = 0;
+        int k = 0, kprev = 0, y = 0;
+        unsigned long long cnt = 0, lo = 0, cb[2] = {0, 0};  // as in po_levels_kernel
         for (int L = 0;; L++) {
             int par = L & 1;
             Ctrl hc;
@@ -572,14 +606,19 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
             if (L > 0) { po_close_kernel<<<1, 1, 0, s>>>(a, par ^ 1, kprev); launches++; }
             if (hc.nAlive[par] == 0) break;
             k = std::max(k + 1, hc.kminb[par]);
-            unsigned long long lstart = hc.q_tail, lo = lstart;
-            po_scan_kernel<STATS><<<blocks, 512, 0, s>>>(a, k, par);
+            const unsigned long long lstart = lo;
+            po_scan_kernel<STATS><<<blocks, 512, 0, s>>>(a, k, par, PoAppend{lo, cb[y], y});
             launches++;
             for (int sub = 0;; sub++) {
-                if ((err = cudaMemcpyAsync(&tail, &a.ctl->q_tail, sizeof(tail), cudaMemcpyDeviceToHost, s)))
+                if ((err = cudaMemcpyAsync(&cnt, y ? &a.ctl->q_tail1 : &a.ctl->q_tail, sizeof(cnt),
+                                           cudaMemcpyDeviceToHost, s)))
                     return err;
                 if ((err = cudaStreamSynchronize(s))) return err;
-                if (tail == lo) {
+                const unsigned long long hi = lo + (cnt - cb[y]);
+                cb[y] = cnt;
+                y ^= 1;
+                if (hi == lo) {
+                    y ^= 1;
                     if (sub == 0) {  // empty level: still consume alive[par]
                         unsigned long long z = 0;
                         int imax = INT_MAX;
@@ -588,10 +627,10 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
                     }
                     break;
                 }
-                po_sub_kernel<MODE, STATS><<<blocks, 512, 0, s>>>(a, k, par, lo, tail, sub == 0);
+                po_sub_kernel<MODE, STATS><<<blocks, 512, 0, s>>>(a, k, par, PoAppend{hi, cb[y], y}, lo, hi, sub == 0);
                 launches++;
                 host_subrounds++;
-                lo = tail;
+                lo = hi;
             }
             if (CLAMP_SUB && lo > lstart) {
                 po_repair_kernel<<<blocks, 512, 0, s>>>(a, k, lstart, lo);
@@ -623,7 +662,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         st->levels = (int64_t)hc.levels;
         st->subrounds = (flags & PICO_F_HOST_LOOP) ? host_subrounds : (int64_t)hc.rounds;
         st->kmax = hc.kmax;
-        st->segments = (int64_t)hc.q_tail;
+        st->segments = (int64_t)(hc.q_tail + hc.q_tail1);
         st->kernel_count += launches;
         if (st->frontier_sizes)
             for (unsigned long long i = 0; i < hc.levels && (int64_t)i < st->frontier_sizes_cap && i < kFszCap; i++)

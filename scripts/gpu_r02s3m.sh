@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+sed -n '/^cat > \/tmp\/po_ab.py/,/^PY$/p' scripts/gpu_r02s3h.sh | sed '1d;$d' > /tmp/po_ab.py
+for rep in 1 2; do
+for v in base flip; do
+  PICO_LIB=build_variants/libpico_$v.so timeout 600 python /tmp/po_ab.py C2 C3 T C4 2>&1 | tail -1
+done
+done
