@@ -16,6 +16,7 @@ from .coreness import (  # noqa: F401
     bz,
     hindex,
     jacobi_rounds,
+    frontier_counts,
     peel_levels,
     kcore_check,
     brute_coreness,

@@ -41,6 +41,9 @@ def _load():
         lib.oracle_hindex.restype = ctypes.c_int64
         lib.oracle_jacobi_rounds.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P, _I64P, ctypes.c_int64]
         lib.oracle_jacobi_rounds.restype = ctypes.c_int64
+        lib.oracle_frontier_counts.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P,
+                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        lib.oracle_frontier_counts.restype = ctypes.c_int64
         lib.oracle_peel_levels.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P, _I64P, _I64P]
         lib.oracle_peel_levels.restype = ctypes.c_int64
         lib.oracle_kcore_check.argtypes = [_I64P, _I32P, ctypes.c_int64, _I32P]
@@ -105,6 +108,26 @@ def jacobi_rounds(rowptr, colidx, max_record: int = 1 << 16):
     if l2 < 0:
         raise MemoryError("oracle_jacobi_rounds allocation failed")
     return core[:n], int(l2), [int(x) for x in fs[: min(l2, max_record)]]
+
+
+def frontier_counts(rowptr, colidx):
+    """The paper's Fig 3 measure on the synchronous sweeps:
+    returns (fcount, l2, nbr_unchanged, nbr_total) -- fcount[v] = the sweeps
+    in which v is a frontier (an edge {u, v} is read fcount[u] + fcount[v]
+    times), and the frontier-neighbour pairs whose neighbour's estimate stays
+    unchanged in the next sweep, out of all such pairs."""
+    rp, ci = _csr(rowptr, colidx)
+    n = rp.size - 1
+    fc = np.zeros(max(n, 1), dtype=np.int32)
+    un = ctypes.c_int64(0)
+    tot = ctypes.c_int64(0)
+    if n == 0:
+        return fc[:0], 0, 0, 0
+    l2 = _load().oracle_frontier_counts(rp.ctypes.data_as(_I64P), ci.ctypes.data_as(_I32P), n,
+                                        fc.ctypes.data_as(_I32P), ctypes.byref(un), ctypes.byref(tot))
+    if l2 < 0:
+        raise MemoryError("oracle_frontier_counts allocation failed")
+    return fc[:n], int(l2), int(un.value), int(tot.value)
 
 
 def peel_levels(rowptr, colidx):

@@ -239,6 +239,76 @@ def test_jacobi_vs_python_sweeps(oracle_mod):
         assert l2 == len(psz) and fs == psz
 
 
+def _py_frontier_counts(n, rp, ci, hfun):
+    """Independent Fig 3 measure: per-vertex frontier multiplicity
+    and the (frontier, neighbour) pairs whose neighbour stays unchanged in the
+    next sweep, from plain Python sweeps with the sort-based h-index."""
+    cur = [int(rp[v + 1] - rp[v]) for v in range(n)]
+    fc = [0] * n
+    front = []
+    un = tot = 0
+    while True:
+        nxt = [hfun([cur[ci[e]] for e in range(rp[v], rp[v + 1])]) for v in range(n)]
+        for v in front:
+            for e in range(rp[v], rp[v + 1]):
+                tot += 1
+                un += nxt[ci[e]] == cur[ci[e]]
+        front = [v for v in range(n) if nxt[v] != cur[v]]
+        if not front:
+            return fc, un, tot
+        for v in front:
+            fc[v] += 1
+        cur = nxt
+
+
+def test_frontier_counts_vs_python(oracle_mod):
+    """oracle_frontier_counts (the Fig 3 measure) against an independent
+    Python sweep on 150 random graphs; its sum is the sum of the pinned |F_t|
+    of oracle_jacobi_rounds and its l2 the same."""
+    rng = random.Random(78)
+    for _ in range(150):
+        n = rng.randint(2, 60)
+        p = rng.choice([0.05, 0.1, 0.3, 0.6])
+        e = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        rp, ci = csr_np(n, e)
+        fc, l2, un, tot = oracle_mod.frontier_counts(rp, ci)
+        pfc, pun, ptot = _py_frontier_counts(n, rp, ci, oracle_mod.hindex_sorted)
+        assert list(fc) == pfc and (un, tot) == (pun, ptot)
+        _, jl2, fs = oracle_mod.jacobi_rounds(rp, ci)
+        assert l2 == jl2 and int(fc.sum()) == sum(fs)
+
+
+def test_frontier_counts_closed_forms(oracle_mod):
+    """Closed forms: a star K_1,k (k >= 2) changes only its centre, once (deg
+    k -> 1); K_n never changes; P5 = 0-1-2-3-4 changes 1 and 3 in sweep 1
+    (h-index of {1, 2} = 1) and 2 in sweep 2 (neighbours now {1, 1}); of the
+    sweep-1 frontier's neighbour pairs (1: {0, 2}, 3: {2, 4}) only those to 2
+    see a change in sweep 2.  G1 (l2 = 1): the frontier is {v : h1 < deg}."""
+    from conftest import parse_g1
+    for k in (2, 3, 7):
+        rp, ci = csr_np(k + 1, [(0, i) for i in range(1, k + 1)])
+        fc, l2, un, tot = oracle_mod.frontier_counts(rp, ci)
+        assert list(fc) == [1] + [0] * k and l2 == 1
+        assert tot == k and un == k  # the leaves' estimates stay 1
+    rp, ci = csr_np(5, [(i, j) for i in range(5) for j in range(i + 1, 5)])
+    fc, l2, un, tot = oracle_mod.frontier_counts(rp, ci)
+    assert list(fc) == [0] * 5 and l2 == 0 and tot == 0
+    rp, ci = csr_np(5, [(0, 1), (1, 2), (2, 3), (3, 4)])
+    fc, l2, un, tot = oracle_mod.frontier_counts(rp, ci)
+    assert list(fc) == [0, 1, 1, 1, 0] and l2 == 2
+    # sweep-1 frontier {1, 3}: pairs (1,0) (1,2) (3,2) (3,4); in sweep 2 only 2 changes;
+    # sweep-2 frontier {2}: pairs (2,1) (2,3), unchanged in the (empty) sweep 3
+    assert tot == 6 and un == 4
+    g = parse_g1()
+    edges = [tuple(int(x) for x in p.split("-")) for p in g["edges"].split()]
+    n = 1 + max(max(e) for e in edges)
+    rp, ci = csr_np(n, edges)
+    fc, l2, _, _ = oracle_mod.frontier_counts(rp, ci)
+    deg = np.diff(rp)
+    h1 = [oracle_mod.hindex([int(deg[u]) for u in ci[rp[v]:rp[v + 1]]]) for v in range(n)]
+    assert l2 == 1 and list(fc) == [int(h1[v] < deg[v]) for v in range(n)]
+
+
 def test_jacobi_fixed_point_and_monotone(oracle_mod):
     """Fixed point HINDEX(core(nbr v)) == core(v); estimates only
     decrease so every |F_t| <= n."""
