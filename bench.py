@@ -322,10 +322,12 @@ def measure_algo(pico, rp, ci, algo: str, args, stream, flush_bytes: int, peak: 
     st = pico.Stats()
     fs = np.zeros(1 << 16, dtype=np.int64)
     ra = np.zeros(1 << 16, dtype=np.int64)
+    fcnt = np.zeros(max(n, 1), dtype=np.int32) if algo == "histocore" else None
     core = pico.coreness(rp, ci, algo=algo, flags=pico.F_STATS | args.flags, stats=st,
-                         frontier_sizes=fs, round_arcs=ra)
+                         frontier_sizes=fs, round_arcs=ra, frontier_counts=fcnt)
     torch.cuda.synchronize()
     sd = st.to_dict()
+    fig3 = fig3_summary(rp, ci, fcnt[:n]) if fcnt is not None else None
     # per-kernel times: a separate instrumented pass (events created per launch slot)
     acc = {"ms": {}, "n": 0}
 
@@ -393,7 +395,43 @@ def measure_algo(pico, rp, ci, algo: str, args, stream, flush_bytes: int, peak: 
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if fig3 is not None:
+        res["fig3"] = fig3
     return core, res
+
+
+def fig3_summary(rp, ci, fcnt):
+    """The paper's Fig 3 measure from the library's per-vertex
+    frontier counts (PICO_F_STATS, pico_stats_t.frontier_counts): the share of
+    (non-isolated) vertices that are a frontier more than 2 times, and of edges
+    read more than 2 / more than 5 times (an edge {u, v} is read once per round
+    in which u or v is a frontier: f(u) + f(v) times).  Arcs are counted on
+    the GPU in chunks (each undirected edge appears twice, with the same
+    count, so arc shares are edge shares)."""
+    import torch
+    dev = rp.device
+    f = torch.from_numpy(fcnt).to(dev)
+    deg = rp[1:] - rp[:-1]
+    live = deg > 0
+    nl = int(live.sum())
+    out = {"vertices_frontier_ge1": float(((f >= 1) & live).sum()) / max(nl, 1),
+           "vertices_frontier_gt2": float(((f > 2) & live).sum()) / max(nl, 1),
+           "vertices_frontier_max": int(f.max()) if f.numel() else 0}
+    arcs = ci.numel()
+    gt2 = gt5 = 0
+    step = 1 << 27
+    for s0 in range(0, arcs, step):
+        e = torch.arange(s0, min(arcs, s0 + step), dtype=torch.int64, device=dev)
+        u = torch.searchsorted(rp, e, right=True) - 1
+        acc = f[u] + f[ci[s0:s0 + e.numel()].long()]
+        gt2 += int((acc > 2).sum())
+        gt5 += int((acc > 5).sum())
+        del e, u, acc
+    out["edges_read_gt2"] = gt2 / max(arcs, 1)
+    out["edges_read_gt5"] = gt5 / max(arcs, 1)
+    out["paper_soc_twitter_2010"] = {"vertices_frontier_gt2": 0.189, "edges_read_gt2": 0.88,
+                                     "edges_read_gt5": 0.609, "source": "P:228-231"}
+    return out
 
 
 def bench_single(args):

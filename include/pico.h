@@ -201,6 +201,13 @@ typedef struct {
      * restricted BFS set R) and that BFS's levels */
     int64_t affected;
     int64_t bfs_levels;
+    /* optional caller-owned HOST int32 array of frontier_counts_cap >= n
+     * entries receiving, for HistoCore with PICO_F_STATS, the number of
+     * rounds in which each vertex was a frontier (its estimate changed) --
+     * the measure of the paper's Fig 3: an edge {u, v} is read
+     * frontier_counts[u] + frontier_counts[v] times; may be NULL */
+    int32_t *frontier_counts;
+    int64_t frontier_counts_cap;
 } pico_stats_t;
 
 /* The north-star entry point: coreness of every vertex, device buffers. */

@@ -44,7 +44,8 @@ def workspace_bytes(n: int, m: int, algo="histocore", flags: int = 0) -> int:
 
 
 def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspace=None,
-             stats: Stats | None = None, frontier_sizes=None, round_arcs=None, round_ns=None, stream=None):
+             stats: Stats | None = None, frontier_sizes=None, round_arcs=None, round_ns=None, stream=None,
+             frontier_counts=None):
     """Coreness of every vertex of a symmetric deduplicated CSR graph held in
     device memory (``pico_coreness_ex``).
 
@@ -53,7 +54,10 @@ def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspa
     in place; ``frontier_sizes`` an optional int64 numpy array receiving
     |F_t| per round (HistoCore) or vertices per level (PeelOne);
     ``round_arcs`` / ``round_ns`` (2 entries per round: UpdateHisto, SumHisto
-    device ns) optional int64 numpy arrays for HistoCore.
+    device ns) optional int64 numpy arrays for HistoCore.  ``frontier_counts``
+    (HistoCore, needs PICO_F_STATS): an optional int32 numpy array of >= n
+    entries receiving each vertex's number of frontier rounds (the paper's
+    Fig 3 measure).
     """
     import torch
     lib = load()
@@ -81,6 +85,14 @@ def coreness(rowptr, colidx, algo="histocore", flags: int = 0, out=None, workspa
     if workspace is not None:
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     st = stats
+    if frontier_counts is not None:
+        if not (isinstance(frontier_counts, np.ndarray) and frontier_counts.dtype == np.int32
+                and frontier_counts.flags.c_contiguous and frontier_counts.size >= n):
+            raise ValueError(f"frontier_counts must be a C-contiguous int32 numpy array of >= {n} entries")
+        if st is None:
+            st = Stats()
+        st.frontier_counts = frontier_counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        st.frontier_counts_cap = frontier_counts.size
     if frontier_sizes is None and (round_arcs is not None or round_ns is not None):
         raise ValueError("round_arcs / round_ns need frontier_sizes (their capacity is its size)")
     if frontier_sizes is not None:

@@ -69,6 +69,8 @@ class Stats(ctypes.Structure):
         ("algo", ctypes.c_int64),
         ("affected", ctypes.c_int64),
         ("bfs_levels", ctypes.c_int64),
+        ("frontier_counts", ctypes.POINTER(ctypes.c_int32)),
+        ("frontier_counts_cap", ctypes.c_int64),
     ]
 
     def to_dict(self) -> dict:

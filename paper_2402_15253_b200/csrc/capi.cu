@@ -150,12 +150,15 @@ cudaError_t pico::lib_malloc_async(void **p, size_t bytes, cudaStream_t s) {
 static void reset_stats(pico_stats_t *st) {
     if (!st) return;
     int64_t *fs = st->frontier_sizes, *ra = st->round_arcs, *rn = st->round_ns;
-    int64_t cap = st->frontier_sizes_cap;
+    int64_t cap = st->frontier_sizes_cap, fcap = st->frontier_counts_cap;
+    int32_t *fc = st->frontier_counts;
     memset(st, 0, sizeof(*st));
     st->frontier_sizes = fs;
     st->frontier_sizes_cap = cap;
     st->round_arcs = ra;
     st->round_ns = rn;
+    st->frontier_counts = fc;
+    st->frontier_counts_cap = fcap;
 }
 
 extern "C" {
@@ -298,6 +301,8 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
     }
     if (rc == PICO_OK) {
         if (m == 0) {
+            if (stats && stats->frontier_counts && stats->frontier_counts_cap >= n)  // no round: no frontier
+                memset(stats->frontier_counts, 0, sizeof(int32_t) * (size_t)n);
             e = cudaMemsetAsync(core_out, 0, sizeof(int32_t) * (size_t)n, s);
             if (!e) e = cudaStreamSynchronize(s);
             if (e) rc = cuda_fail(e, "zero core_out");
@@ -356,6 +361,18 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
                 if (timing) cudaEventRecord(b1, s);
                 if (!e) e = cudaStreamSynchronize(s);
                 if (e) rc = cuda_fail(e, "relabel back");
+                if (rc == PICO_OK && algo == PICO_ALGO_HISTOCORE && stats && stats->frontier_counts &&
+                    (flags & PICO_F_STATS) && stats->frontier_counts_cap >= n) {
+                    // the counts came back in compacted ids 0..n2-1: to original ids
+                    std::vector<int> inv((size_t)rl.n2), tmp((size_t)rl.n2);
+                    e = cudaMemcpy(inv.data(), rl.inv, sizeof(int) * (size_t)rl.n2, cudaMemcpyDeviceToHost);
+                    if (e) rc = cuda_fail(e, "relabel back (frontier counts)");
+                    else {
+                        memcpy(tmp.data(), stats->frontier_counts, sizeof(int) * (size_t)rl.n2);
+                        memset(stats->frontier_counts, 0, sizeof(int) * (size_t)n);
+                        for (long long i = 0; i < rl.n2; i++) stats->frontier_counts[inv[(size_t)i]] = tmp[(size_t)i];
+                    }
+                }
                 if (stats) stats->kernel_count += rl.launches + 1;
                 if (timing && rc == PICO_OK) {
                     float t1 = 0, t2 = 0;

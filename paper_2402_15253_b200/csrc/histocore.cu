@@ -146,6 +146,9 @@ struct HcArgs {
     // 32-bit copy of rowptr when 2m < 2^32 (null otherwise): the histogram-base
     // gathers of UpdateHisto / SumHisto read half the bytes
     unsigned *rp32;
+    // PICO_F_STATS with pico_stats_t.frontier_counts: rounds in which each
+    // vertex was a frontier (the paper's Fig 3 measure); null: off
+    int *fcnt = nullptr;
 };
 
 // rowptr[v] through the 32-bit copy when there is one (uniform branch)
@@ -220,6 +223,7 @@ struct ChangeAcc {
         arcs += d;
         kmin = min(kmin, k);
         atomicOr(a.chg + (t & 1) * a.nwords + (v >> 5), 1u << (v & 31));
+        if (a.fcnt) a.fcnt[v]++;  // one lane handles v per round
     }
     // all 32 lanes call; count_into: counter of |C_t| (init only) or null
     __device__ __forceinline__ void flush(const HcArgs &a, int t, unsigned long long *count_into) {
@@ -589,6 +593,7 @@ __device__ bool cta_init_vertex(const HcArgs &a, int v, int *bins, int *red, int
             atomicAdd(&a.ctl->arcsC[1], (unsigned long long)d);
             atomicMin(&a.ctl->mincv[1], h);
             atomicOr(a.chg + a.nwords + (v >> 5), 1u << (v & 31));
+            if (a.fcnt) a.fcnt[v]++;
             if (ns) red[34] = (int)atomicAdd(&a.ctl->nS[1], (unsigned long long)ns);
         }
         if (STATS) {
@@ -1427,7 +1432,7 @@ static int hc_npass(long long n, uint32_t flags, int rb = 4) {
 }
 
 struct HcLayout {
-    size_t ctl, fsz, rarcs, rtime, histo, c8, c16, rec, e16, rp32, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
+    size_t fcnt, ctl, fsz, rarcs, rtime, histo, c8, c16, rec, e16, rp32, oldc, F, BC, S, H, chg, ro, db, slen, capd, bk, psrc, pdst,
         elc, elt, total;
     long long nwords, scap, hcap, nbcap;
     size_t eltb;
@@ -1466,6 +1471,7 @@ static HcLayout hc_layout(long long n, long long arcs, uint32_t flags, long long
     L.db = b; b += align256((size_t)n);
     L.slen = b; b += align256(sizeof(int) * (size_t)n);
     L.capd = b; b += align256(sizeof(unsigned) * (size_t)L.nwords);
+    L.fcnt = b; b += align256(sizeof(int) * (size_t)((flags & PICO_F_STATS) ? std::max(n, 1ll) : 1));
     const size_t el = pull ? (size_t)std::max(arcs, 1ll) : 1;  // pull edge list
     L.bk = b; b += align256(sizeof(unsigned long long) * (kMaxPass + 1));
     L.psrc = b; b += align256(sizeof(int) * el);
@@ -1575,6 +1581,8 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     a.nv16 = a.c16;
     a.nv32 = a.oldc;
     a.prefilter = (flags & PICO_F_PREFILTER) ? 1 : 0;
+    const bool fcounts = STATS && st && st->frontier_counts && st->frontier_counts_cap >= n && !keep;
+    if (fcounts) a.fcnt = (int *)(p + L.fcnt);
 
     Timer tm{s, (flags & PICO_F_TIMING) != 0, {}};
     cudaError_t err;
@@ -1583,6 +1591,7 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     if ((err = cudaMemcpyAsync(a.ctl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
     if ((err = cudaMemsetAsync(a.chg, 0, sizeof(unsigned) * 2 * (size_t)L.nwords, s))) return err;
     if ((err = cudaMemsetAsync(a.capd, 0, sizeof(unsigned) * (size_t)L.nwords, s))) return err;
+    if (fcounts && (err = cudaMemsetAsync(a.fcnt, 0, sizeof(int) * (size_t)n, s))) return err;
 
     const int sms = dev.sms;
     long long launches = 0;
@@ -1813,6 +1822,11 @@ static cudaError_t hc_run_t(const long long *rp, const int *ci, long long n, lon
     if (st) {
         st->rounds = (int64_t)rounds;
         st->kernel_count += launches;
+        if (fcounts) {
+            if ((err = cudaMemcpyAsync(st->frontier_counts, a.fcnt, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, s)))
+                return err;
+            if ((err = cudaStreamSynchronize(s))) return err;
+        }
         st->segments_init = (int64_t)s1;
         if (st->frontier_sizes)
             for (size_t i = 0; i < hsz.size() && (int64_t)i < st->frontier_sizes_cap; i++)

@@ -286,3 +286,30 @@ def test_debug_invariants():
         for fl in (0, pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS | pico.F_TINY_TILES, pico.F_HOST_LOOP):
             core, _, _ = _run(rp, ci, "histocore", fl | pico.F_DEBUG_INVARIANTS)
             assert np.array_equal(core, ref)
+
+
+def test_frontier_counts_fig3():
+    """pico_stats_t.frontier_counts (PICO_F_STATS): the rounds in which each
+    vertex is a frontier -- the paper's Fig 3 measure -- equal the
+    oracle's synchronous sweeps vertex by vertex, in every schedule (push,
+    pull, tiny tiles, host loop) and through the compaction (F_RELABEL maps the
+    counts back to the original ids)."""
+    pico = _pico()
+    graphs = [("R12", synth.to_numpy(*synth.CONFIGS["R12"].build())),
+              ("C1", synth.to_numpy(*synth.CONFIGS["C1"].build())),
+              ("chung-lu", synth.to_numpy(*synth.chung_lu(3000, 8.0, 2.3, seed=5)))]
+    for name, (rp, ci) in graphs:
+        ref, l2, _, _ = oracle.frontier_counts(rp, ci)
+        n = rp.size - 1
+        for fl in (0, pico.F_PUSH_ONLY, pico.F_PULL_ALWAYS, pico.F_PULL_ALWAYS | pico.F_TINY_TILES,
+                   pico.F_HOST_LOOP, pico.F_RELABEL, pico.F_RELABEL | pico.F_PULL_ALWAYS):
+            import torch
+            dev = torch.device("cuda:0")
+            fc = np.full(n + 3, -7, dtype=np.int32)
+            st = pico.Stats()
+            core = pico.coreness(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), algo="histocore",
+                                 flags=fl | pico.F_STATS, stats=st, frontier_counts=fc)
+            torch.cuda.synchronize()
+            assert st.rounds == l2, (name, fl)
+            assert np.array_equal(fc[:n], ref), (name, fl, int(np.flatnonzero(fc[:n] != ref)[0]))
+            assert np.array_equal(core.cpu().numpy(), oracle.bz(rp, ci))
