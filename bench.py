@@ -529,6 +529,8 @@ def bench_single(args):
             entry[algo]["frac"] = res["roofline"]["frac"]
             entry[algo]["whole_step_frac"] = res["roofline"]["whole_step_frac"]
             entry[algo]["kernel"] = res["roofline"]["kernel"]
+            if "fig3" in res:
+                entry[algo]["fig3"] = {k: v for k, v in res["fig3"].items() if k != "paper_soc_twitter_2010"}
             if algo == "peelone":
                 entry[algo]["agrees_with_histocore"] = bool(np.array_equal(cn, cref))
             log(f"[bench] {c} {algo}: {res['ms']:.3f} ms/step, frac {res['roofline']['frac']:.3f}")
