@@ -101,7 +101,7 @@ def bench_sharded(args):
         try:
             comm = sharded.NcclComm()
             exchange_note = "NCCL inside libpico (pico_coreness_sharded)"
-            if args.exchange == "lsa" and args.algo != "peelone":
+            if args.exchange == "lsa":
                 args.flags |= pico.F_LSA_EXCHANGE
                 exchange_note = ("NCCL device API inside libpico (symmetric window, LSA peer loads, one LSA "
                                  "barrier per round, no host synchronisation per round)")

@@ -123,8 +123,8 @@ enum {
                               /* pico_relabel_threshold() and >= 10% of the  */
                               /* ids are isolated, so per-vertex arrays fit  */
                               /* the L2; PeelOne compacts only when forced)  */
-    PICO_F_LSA_EXCHANGE = 32768u /* pico_coreness_sharded_ex, HistoCore: the */
-                              /* per-round exchange on the device through    */
+    PICO_F_LSA_EXCHANGE = 32768u /* pico_coreness_sharded_ex (HistoCore and  */
+                              /* PeelOne): the exchange on the device through */
                               /* NCCL's device API (symmetric window, LSA    */
                               /* peer loads, one LSA barrier per round), no  */
                               /* host synchronisation per round; needs NCCL  */

@@ -172,7 +172,11 @@ int pico_coreness_sharded(pico_comm_t comm, const int64_t *rowptr_local, const i
  * the peers' triples over NVLink in rank order; the host enqueues rounds in
  * batches (PICO_LSA_BATCH, default 4) and reads the global counts once per
  * batch (rounds after convergence are empty no-ops).  Same coreness, l2 and
- * |C_t| as the host exchange.  PICO_ENOTSUP (nothing computed) when the
+ * |C_t| as the host exchange.  PeelOne with the flag: the level loop itself
+ * runs on the device (one thread decides scan / apply / done after every
+ * exchange of (|F|, next-level bound) pairs and F), batches of 16 steps are
+ * one CUDA graph, and the host reads a done flag per batch; same levels,
+ * sub-rounds and k_max.  PICO_ENOTSUP (nothing computed) when the
  * loaded NCCL lacks the device API or the ranks are not one LSA team. */
 int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
                              int64_t n_global, int64_t m_global, int64_t v_begin, int64_t v_end, int algo,

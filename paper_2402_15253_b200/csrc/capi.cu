@@ -825,13 +825,13 @@ static int lsa_rounds(pico_comm_t comm, Shard *sh, const std::vector<long long> 
     for (int r = 0; r < P; r++) cap = std::max(cap, hm[3 * r + 1] - hm[3 * r]);
     std::string msg;
     cudaError_t e = cudaSuccess;
-    if (!comm->lsa || comm->lsa_cap < cap) {  // the same decision on every rank (cap is global)
+    if (!comm->lsa || comm->lsa_cap < cap || lsa_words(comm->lsa) != 3) {  // the same decision on every rank
         if (comm->lsa) {
             if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "LSA exchange setup");
             lsa_destroy(comm->lsa);
             comm->lsa = nullptr;
         }
-        e = lsa_create((void *)comm->c, P, me, cap, &comm->lsa, &msg);
+        e = lsa_create((void *)comm->c, P, me, cap, 3, &comm->lsa, &msg);
         if (e == cudaErrorNotSupported) return fail(PICO_ENOTSUP, "LSA exchange unavailable: %s", msg.c_str());
         if (e) return msg.empty() ? cuda_fail(e, "LSA exchange setup") : fail(PICO_ENCCL, "%s", msg.c_str());
         comm->lsa_cap = cap;
@@ -876,6 +876,43 @@ static int lsa_rounds(pico_comm_t comm, Shard *sh, const std::vector<long long> 
     cudaError_t es = cudaStreamSynchronize(s);
     if (rc == PICO_OK && es) rc = cuda_fail(es, "LSA cleanup");
     return rc;
+}
+
+// sharded PeelOne with the level loop on the device and the exchange over
+// NCCL's device API (PICO_F_LSA_EXCHANGE; shard_peel.cu pshard_run_lsa)
+static int peel_rounds_lsa(pico_comm_t comm, PeelShard *ps, const std::vector<long long> &hm, long long n_global,
+                           int32_t *core_out_local, long long nloc, pico_stats_t *stats, cudaStream_t s) {
+    const int P = comm->nranks, me = comm->rank;
+    long long cap = 1;
+    for (int r = 0; r < P; r++) cap = std::max(cap, hm[3 * r + 1] - hm[3 * r]);
+    std::string msg;
+    cudaError_t e = cudaSuccess;
+    if (!comm->lsa || comm->lsa_cap < cap || lsa_words(comm->lsa) != 1) {  // the same decision on every rank
+        if (comm->lsa) {
+            if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "LSA exchange setup");
+            lsa_destroy(comm->lsa);
+            comm->lsa = nullptr;
+        }
+        e = lsa_create((void *)comm->c, P, me, cap, 1, &comm->lsa, &msg);
+        if (e == cudaErrorNotSupported) return fail(PICO_ENOTSUP, "LSA exchange unavailable: %s", msg.c_str());
+        if (e) return msg.empty() ? cuda_fail(e, "LSA exchange setup") : fail(PICO_ENCCL, "%s", msg.c_str());
+        comm->lsa_cap = cap;
+    }
+    long long levels = 0, subrounds = 0;
+    int kmax = 0;
+    std::vector<long long> lv;
+    long long lvcap = (stats && stats->frontier_sizes) ? stats->frontier_sizes_cap : 0;
+    lv.resize((size_t)std::max(lvcap, 1ll));
+    e = pshard_run_lsa(ps, comm->lsa, n_global, &levels, &subrounds, &kmax, lvcap ? lv.data() : nullptr, lvcap, &msg);
+    if (e) return msg.empty() ? cuda_fail(e, "sharded PeelOne (LSA)") : fail(PICO_EGRAPH, "%s", msg.c_str());
+    if (stats) {
+        stats->levels = levels;
+        stats->subrounds = subrounds;
+        stats->kmax = kmax;
+        for (long long i = 0; i < std::min(levels, lvcap); i++) stats->frontier_sizes[i] = lv[(size_t)i];
+    }
+    if (nloc > 0 && (e = pshard_result(ps, core_out_local))) return cuda_fail(e, "shard result");
+    return PICO_OK;
 }
 
 int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, const int32_t *colidx_local,
@@ -942,6 +979,10 @@ int pico_coreness_sharded_ex(pico_comm_t comm, const int64_t *rowptr_local, cons
         }
         if (!tiled) { rc = fail(PICO_EINVAL, "rank ranges do not tile [0, n_global) in rank order"); break; }
         if (arcs != 2 * m_global) { rc = fail(PICO_EINVAL, "local arcs sum to %lld, not 2m = %lld", arcs, 2 * (long long)m_global); break; }
+        if (peel && (flags & PICO_F_LSA_EXCHANGE)) {
+            rc = peel_rounds_lsa(comm, ps, hm, n_global, core_out_local, nloc, stats, s);
+            break;
+        }
         if (peel) {
             rc = peel_rounds(comm, ps, nloc, trip, all, all_cap, cnt, core_out_local, stats, s);
             break;

@@ -1,6 +1,7 @@
 // kernels.h -- internal host-side interface between the C ABI (capi.cu) and
 // the algorithm drivers (histocore.cu, peelone.cu, shard.cu).
 #pragma once
+#include <string>
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -88,6 +89,11 @@ cudaError_t pshard_read(PeelShard *h, long long *count, int *kmin);
 cudaError_t pshard_counters(PeelShard *h, long long *arcs_scanned, long long *guarded);
 cudaError_t pshard_result(PeelShard *h, int *core_out);
 cudaError_t pshard_destroy(PeelShard *h);
+// the level loop driven on the device, exchanging over NCCL's device API
+// (PICO_F_LSA_EXCHANGE; lx: a window of 1-word items, cap >= every rank's nloc)
+struct LsaX;
+cudaError_t pshard_run_lsa(PeelShard *h, LsaX *lx, long long n_global, long long *levels, long long *subrounds,
+                           int *kmax, long long *lvsz_host, long long lvcap, std::string *msg);
 
 // decremental HistoCore (histocore.cu)
 struct Dyn;

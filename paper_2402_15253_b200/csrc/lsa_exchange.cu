@@ -29,6 +29,7 @@
 // returns an error).
 #include <dlfcn.h>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <string>
 
@@ -95,7 +96,8 @@ static NcclDevApi &dev_api() {
 struct LsaX {
     ncclComm_t comm = nullptr;
     int P = 0, me = 0;
-    long long cap = 0;           // triples per rank and parity
+    long long cap = 0;           // items per rank and parity
+    int words = 3;               // int32 words per item (3: HistoCore triples, 1: PeelOne ids)
     void *buf = nullptr;         // the symmetric window's memory (ncclMemAlloc)
     size_t bytes = 0;
     ncclWindow_t win = nullptr;
@@ -105,45 +107,55 @@ struct LsaX {
 };
 
 static size_t a4k(size_t x) { return (x + 4095) & ~size_t(4095); }
-static size_t cnt_off(const LsaX *x, int parity) { return sizeof(unsigned long long) * (size_t)parity * x->P; }
-static size_t trip_base(const LsaX *x) { return a4k(sizeof(unsigned long long) * 2 * (size_t)x->P); }
+// count rows: [parity][rank] (count, aux) int64 pairs
+static size_t cnt_off(const LsaX *x, int parity) { return 2 * sizeof(long long) * (size_t)parity * x->P; }
+static size_t trip_base(const LsaX *x) { return a4k(2 * sizeof(long long) * 2 * (size_t)x->P); }
 static size_t trip_off(const LsaX *x, int parity) {
-    return trip_base(x) + sizeof(int) * 3 * (size_t)x->cap * (size_t)parity;
+    return trip_base(x) + sizeof(int) * (size_t)x->words * (size_t)x->cap * (size_t)parity;
 }
 
-// counts of round t: my |C_t| into every peer's row, one LSA barrier, then
-// the offsets (one warp)
+// counts of an exchange: my (count, aux) pair into every peer's row, one LSA
+// barrier, then the item offsets, the global total and the minimum aux (one
+// warp).  mine: the count (aux: mine[1] when has_aux, e.g. PeelOne's bound
+// of the next level, reduced by min)
 __global__ void __launch_bounds__(32) lsa_counts_kernel(ncclDevComm dc, ncclWindow_t win, size_t row_off, int P, int me,
-                                                        const unsigned long long *mine, unsigned long long *off,
-                                                        long long *tot_out) {
-    const unsigned long long c = *mine;
-    for (int r = threadIdx.x; r < P; r += 32)
-        *reinterpret_cast<volatile unsigned long long *>(
-            (char *)ncclGetLsaPointer(win, row_off + sizeof(unsigned long long) * (size_t)me, r)) = c;
+                                                        const unsigned long long *mine, int has_aux,
+                                                        unsigned long long *off, long long *tot_out,
+                                                        long long *min_out) {
+    const long long c = (long long)mine[0], x = has_aux ? (long long)mine[1] : 0;
+    for (int r = threadIdx.x; r < P; r += 32) {
+        volatile long long *dst = reinterpret_cast<volatile long long *>(
+            (char *)ncclGetLsaPointer(win, row_off + 2 * sizeof(long long) * (size_t)me, r));
+        dst[0] = c;
+        dst[1] = x;
+    }
     {
         ncclLsaBarrierSession<ncclCoopWarp> bar(ncclCoopWarp(), dc, ncclTeamTagLsa(), 0);
         bar.sync(ncclCoopWarp(), cuda::memory_order_acq_rel);
     }
     if (threadIdx.x == 0) {
-        const volatile unsigned long long *row =
-            reinterpret_cast<const volatile unsigned long long *>((char *)ncclGetLocalPointer(win, row_off));
+        const volatile long long *row =
+            reinterpret_cast<const volatile long long *>((char *)ncclGetLocalPointer(win, row_off));
         unsigned long long s = 0;
+        long long mn = LLONG_MAX;
         for (int r = 0; r < P; r++) {
             off[r] = s;
-            s += row[r];
+            s += (unsigned long long)row[2 * r];
+            mn = row[2 * r + 1] < mn ? row[2 * r + 1] : mn;
         }
         off[P] = s;
         if (tot_out) *tot_out = (long long)s;
+        if (min_out) *min_out = mn;
     }
 }
 
-// copy of round t: all[3 off[r] + j] = rank r's triple word j (peer loads)
-__global__ void __launch_bounds__(256) lsa_copy_kernel(ncclWindow_t win, size_t trip_off, int P,
+// copy of an exchange: all[w off[r] + j] = rank r's word j (peer loads)
+__global__ void __launch_bounds__(256) lsa_copy_kernel(ncclWindow_t win, size_t trip_off, int P, int w,
                                                        const unsigned long long *off, int *all) {
     __shared__ unsigned long long s_off[65];
     __shared__ const int *s_src[64];
     for (int r = threadIdx.x; r <= P && r <= 64; r += blockDim.x) {
-        s_off[r] = 3ull * off[r];
+        s_off[r] = (unsigned long long)w * off[r];
         if (r < P) s_src[r] = (const int *)ncclGetLsaPointer(win, trip_off, r);
     }
     __syncthreads();
@@ -164,7 +176,7 @@ static cudaError_t nccl_err(ncclResult_t r, const char *where, std::string *msg)
     return cudaErrorUnknown;
 }
 
-cudaError_t lsa_create(void *comm, int P, int me, long long cap, LsaX **out, std::string *msg) {
+cudaError_t lsa_create(void *comm, int P, int me, long long cap, int words, LsaX **out, std::string *msg) {
     *out = nullptr;
     NcclDevApi &N = dev_api();
     if (!N.ok) {
@@ -180,6 +192,7 @@ cudaError_t lsa_create(void *comm, int P, int me, long long cap, LsaX **out, std
     x->P = P;
     x->me = me;
     x->cap = cap > 0 ? cap : 1;
+    x->words = words;
     x->bytes = a4k(trip_off(x, 2));
     ncclResult_t r;
     cudaError_t e;
@@ -208,12 +221,14 @@ cudaError_t lsa_create(void *comm, int P, int me, long long cap, LsaX **out, std
 
 int *lsa_send_buffer(LsaX *x, int parity) { return (int *)((char *)x->buf + trip_off(x, parity)); }
 long long lsa_capacity(const LsaX *x) { return x->cap; }
+int lsa_words(const LsaX *x) { return x->words; }
 const unsigned long long *lsa_total(const LsaX *x) { return x->off + x->P; }
 
 cudaError_t lsa_exchange(LsaX *x, int parity, const unsigned long long *mine, int *all, long long *tot_out,
-                         int copy_blocks, cudaStream_t s) {
-    lsa_counts_kernel<<<1, 32, 0, s>>>(x->dc, x->win, cnt_off(x, parity), x->P, x->me, mine, x->off, tot_out);
-    lsa_copy_kernel<<<copy_blocks, 256, 0, s>>>(x->win, trip_off(x, parity), x->P, x->off, all);
+                         int copy_blocks, cudaStream_t s, int has_aux, long long *min_out) {
+    lsa_counts_kernel<<<1, 32, 0, s>>>(x->dc, x->win, cnt_off(x, parity), x->P, x->me, mine, has_aux, x->off,
+                                       tot_out, min_out);
+    lsa_copy_kernel<<<copy_blocks, 256, 0, s>>>(x->win, trip_off(x, parity), x->P, x->words, x->off, all);
     return cudaGetLastError();
 }
 
@@ -232,15 +247,17 @@ cudaError_t lsa_destroy(LsaX *x) {
 #else  // built without the NCCL device headers: the host exchange only
 
 struct LsaX {};
-cudaError_t lsa_create(void *, int, int, long long, LsaX **out, std::string *msg) {
+cudaError_t lsa_create(void *, int, int, long long, int, LsaX **out, std::string *msg) {
     *out = nullptr;
     if (msg) *msg = "built without the NCCL device API headers (nccl_device.h, NCCL >= 2.28)";
     return cudaErrorNotSupported;
 }
 int *lsa_send_buffer(LsaX *, int) { return nullptr; }
 long long lsa_capacity(const LsaX *) { return 0; }
+int lsa_words(const LsaX *) { return 0; }
 const unsigned long long *lsa_total(const LsaX *) { return nullptr; }
-cudaError_t lsa_exchange(LsaX *, int, const unsigned long long *, int *, long long *, int, cudaStream_t) {
+cudaError_t lsa_exchange(LsaX *, int, const unsigned long long *, int *, long long *, int, cudaStream_t, int,
+                         long long *) {
     return cudaErrorNotSupported;
 }
 cudaError_t lsa_destroy(LsaX *) { return cudaSuccess; }

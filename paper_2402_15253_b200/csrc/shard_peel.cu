@@ -25,12 +25,16 @@
 // on the number of ranks.  PeelOne needs no degree exchange: every decrement
 // lands on the owner of its target.
 #include <climits>
+#include <cstddef>
+#include <cstdlib>
+#include <string>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "lsa_exchange.h"
 
 namespace pico {
 
@@ -41,6 +45,13 @@ struct PsCtl {
     unsigned long long st_arcs, st_dec;
     int kmin[2];                   // lower bound of the next level (by parity)
     long long out[2];              // published: |F| of this rank, kmin bound
+    // device-driven loop (PICO_F_LSA_EXCHANGE, pshard_run_lsa): the latest
+    // exchange's global results and the decision taken from them
+    long long g_total;             // global |F| of the latest exchange
+    long long g_kmin;              // global min of the published bounds
+    int mode;                      // next step: 0 scan, 1 apply, 2 done
+    int kcur, pcur, Lcnt, level_open, kmax;
+    long long processed, levels, subrounds;
 };
 
 struct PeelShard {
@@ -113,8 +124,8 @@ __global__ void ps_begin_kernel(PsCtl *c, int p) {
 }
 
 // P1: scan of the owned alive list at level k -> F (global ids), kept list
-__global__ void ps_scan_kernel(const int *core, const int *alive, int *next, PsCtl *c, int p, int k, long long vb,
-                               int *front) {
+__device__ __forceinline__ void ps_scan_body(const int *core, const int *alive, int *next, PsCtl *c, int p, int k,
+                                             long long vb, int *front) {
     const long long na = (long long)c->nalive[p];
     long long nt = (long long)gridDim.x * blockDim.x;
     long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -137,6 +148,18 @@ __global__ void ps_scan_kernel(const int *core, const int *alive, int *next, PsC
 }
 
 // publish (|F|, kmin bound of parity q) for the exchange; reset the counters
+__global__ void ps_scan_kernel(const int *core, const int *alive, int *next, PsCtl *c, int p, int k, long long vb,
+                               int *front) {
+    ps_scan_body(core, alive, next, c, p, k, vb, front);
+}
+
+// device-driven loop: the step decided on the device (mode 0 = scan)
+__global__ void ps_scan_dev_kernel(const int *core, int *alive0, int *alive1, PsCtl *c, long long vb, int *front) {
+    if (c->mode != 0) return;
+    const int p = c->pcur;
+    ps_scan_body(core, p ? alive1 : alive0, p ? alive0 : alive1, c, p, c->kcur, vb, front);
+}
+
 __global__ void ps_pub_kernel(PsCtl *c, int q) {
     c->out[0] = (long long)c->fcnt;
     c->out[1] = (long long)c->kmin[q];
@@ -146,7 +169,11 @@ __global__ void ps_pub_kernel(PsCtl *c, int q) {
 
 // (received vertex, segment) items over the CSC columns of the received F
 __global__ void ps_segments_kernel(const int *all, long long total, const long long *csc_off, int seg, int2 *TS,
-                                   unsigned long long *nts) {
+                                   unsigned long long *nts, const PsCtl *dc = nullptr) {
+    if (dc) {  // device-driven loop: an apply step (mode 1) over the exchange's total
+        if (dc->mode != 1) return;
+        total = dc->g_total;
+    }
     long long nt = (long long)gridDim.x * blockDim.x;
     long long iters = (total + nt - 1) / nt;
     for (long long it = 0; it < iters; it++) {
@@ -203,7 +230,12 @@ __device__ __forceinline__ int ps_clamp_dec(int *p, int c, int k) {
 template <int MODE, bool STATS>
 __global__ void __launch_bounds__(512) ps_scatter_kernel(const int *all, const int2 *TS, const long long *csc_off,
                                                          const int *csc_idx, int *core, PsCtl *c, int p, int k,
-                                                         long long vb, int seg, int *front) {
+                                                         long long vb, int seg, int *front, int dev = 0) {
+    if (dev) {  // device-driven loop: an apply step (mode 1) of the level decided on the device
+        if (c->mode != 1) return;
+        p = c->pcur;
+        k = c->kcur;
+    }
     const int lane = lane_id();
     const long long nts = (long long)c->nts;
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -315,6 +347,150 @@ cudaError_t pshard_create(const long long *rp, const int *ci, long long nloc, lo
     }
     *out = h;
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Device-driven level loop (PICO_F_LSA_EXCHANGE): every step is decided on the
+// device from the latest exchange -- the host's loop in capi.cu peel_rounds,
+// moved to one thread -- so the host only enqueues steps (a CUDA graph of a
+// batch) and reads the done flag once per batch.
+//   global |F| > 0 in the open level  -> apply (a BSP sub-round)
+//   else: close the level (record it if it processed anything); the global
+//         bound INT_MAX -> done; else scan level max(k + 1, bound)
+// ---------------------------------------------------------------------------
+__global__ void ps_decide_kernel(PsCtl *c, long long *lvsz, long long lvcap) {
+    if (c->mode == 2) return;
+    if (c->level_open && c->g_total > 0) {
+        c->mode = 1;
+        c->processed += c->g_total;
+        c->subrounds++;
+        return;
+    }
+    if (c->level_open && c->processed > 0) {
+        if (c->levels < lvcap) lvsz[c->levels] = c->processed;
+        c->levels++;
+        c->kmax = c->kcur;
+    }
+    c->level_open = 0;
+    if (c->g_kmin >= (long long)INT_MAX) {
+        c->mode = 2;
+        return;
+    }
+    c->kcur = max(c->kcur + 1, (int)c->g_kmin);
+    const int p = c->Lcnt & 1;
+    c->pcur = p;
+    c->Lcnt++;
+    c->nalive[p ^ 1] = 0;  // ps_begin_kernel of the host loop
+    c->kmin[p ^ 1] = INT_MAX;
+    c->fcnt = 0;
+    c->mode = 0;
+    c->level_open = 1;
+    c->processed = 0;
+}
+
+// publish (|F|, next-level bound) of the step; a finished run publishes (0, none)
+__global__ void ps_pub_dev_kernel(PsCtl *c) {
+    if (c->mode == 2) {
+        c->out[0] = 0;
+        c->out[1] = (long long)INT_MAX;
+        return;
+    }
+    c->out[0] = (long long)c->fcnt;
+    c->out[1] = (long long)c->kmin[c->pcur ^ 1];
+    c->fcnt = 0;
+    c->nts = 0;
+}
+
+cudaError_t pshard_run_lsa(PeelShard *h, LsaX *lx, long long n_global, long long *levels, long long *subrounds,
+                           int *kmax, long long *lvsz_host, long long lvcap, std::string *msg) {
+    cudaStream_t s = h->s;
+    const int sms = h->dev.sms;
+    cudaError_t e;
+    int *all = nullptr;
+    long long *lvsz = nullptr;
+    const long long lv_dev_cap = std::max(lvcap, 1ll);
+    int batch = 16;  // even: a batch's exchange parities repeat
+    if (const char *b = getenv("PICO_LSA_BATCH")) batch = std::max(2, std::min(256, atoi(b) & ~1));
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaStream_t cs = nullptr;
+    do {
+        if ((e = lib_malloc_async(&all, sizeof(int) * (size_t)std::max(n_global, 1ll), s))) break;
+        if ((e = lib_malloc_async(&lvsz, sizeof(long long) * (size_t)lv_dev_cap, s))) break;
+        PsCtl *c = h->ctl;
+        // loop state: no level open, k = 0 (the init published (0, kmin0))
+        if ((e = cudaMemsetAsync(&c->g_total, 0, offsetof(PsCtl, subrounds) + sizeof(long long) -
+                                                     offsetof(PsCtl, g_total), s)))
+            break;
+        // exchange 0: the init's published bounds (parity 0)
+        if ((e = lsa_exchange(lx, 0, (const unsigned long long *)c->out, all, &c->g_total, sms * 4, s, 1,
+                              &c->g_kmin)))
+            break;
+        // one batch of steps, captured once on a private stream (the caller's may
+        // be the legacy stream, which cannot capture) and launched on the
+        // caller's: step j of a batch uses parity (j + 1) & 1
+        if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) break;
+        if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed))) break;
+        const bool stats = h->flags & PICO_F_STATS;
+        for (int j = 0; j < batch; j++) {
+            const int par = (j + 1) & 1;
+            int *front = lsa_send_buffer(lx, par);
+            ps_decide_kernel<<<1, 1, 0, cs>>>(c, lvsz, lvcap);
+            if (h->nloc > 0)
+                ps_scan_dev_kernel<<<sms * 4, 512, 0, cs>>>(h->core, h->alive[0], h->alive[1], c, h->vb, front);
+            if (h->arcs > 0) {
+                ps_segments_kernel<<<sms * 16, 256, 0, cs>>>(all, 0, h->csc_off, h->seg, h->TS, &c->nts, c);
+#define PS_LAUNCH_DEV(M, ST) \
+    ps_scatter_kernel<M, ST><<<sms * 4, 512, 0, cs>>>(all, h->TS, h->csc_off, h->csc_idx, h->core, c, 0, 0, h->vb, \
+                                                     h->seg, front, 1)
+                if (h->flags & PICO_F_CLAMP_CAS) {
+                    if (stats) PS_LAUNCH_DEV(2, true); else PS_LAUNCH_DEV(2, false);
+                } else {
+                    if (stats) PS_LAUNCH_DEV(0, true); else PS_LAUNCH_DEV(0, false);
+                }
+#undef PS_LAUNCH_DEV
+            }
+            ps_pub_dev_kernel<<<1, 1, 0, cs>>>(c);
+            if ((e = lsa_exchange(lx, par, (const unsigned long long *)c->out, all, &c->g_total, sms * 4, cs, 1,
+                                  &c->g_kmin)))
+                break;
+        }
+        cudaError_t ec = cudaStreamEndCapture(cs, &g);
+        if (e || (e = ec)) break;
+        if ((e = cudaGraphInstantiate(&ge, g, 0))) break;
+        for (long long nb = 0;; nb++) {
+            if ((e = cudaGraphLaunch(ge, s))) break;
+            int mode = 0;
+            if ((e = cudaMemcpyAsync(&mode, &c->mode, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+                (e = cudaStreamSynchronize(s)))
+                break;
+            if (mode == 2) break;
+            if (nb > (h->arcs + n_global) / batch + 16) {  // every step processes a vertex or a level
+                if (msg) *msg = "sharded PeelOne did not terminate";
+                e = cudaErrorUnknown;
+                break;
+            }
+        }
+        if (e) break;
+        PsCtl hc;
+        if ((e = cudaMemcpyAsync(&hc, c, sizeof(PsCtl), cudaMemcpyDeviceToHost, s)) ||
+            (e = cudaStreamSynchronize(s)))
+            break;
+        *levels = hc.levels;
+        *subrounds = hc.subrounds;
+        *kmax = hc.kmax;
+        if (lvsz_host && hc.levels > 0 &&
+            (e = cudaMemcpy(lvsz_host, lvsz, sizeof(long long) * (size_t)std::min(hc.levels, lvcap),
+                            cudaMemcpyDeviceToHost)))
+            break;
+    } while (false);
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    if (all) cudaFreeAsync(all, s);
+    if (lvsz) cudaFreeAsync(lvsz, s);
+    cudaError_t es = cudaStreamSynchronize(s);
+    return e ? e : es;
 }
 
 const long long *pshard_out(PeelShard *h) { return h->ctl->out; }

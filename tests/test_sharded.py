@@ -453,5 +453,15 @@ def test_sharded_lsa_exchange_single_rank(batch, monkeypatch):
                 torch.cuda.synchronize()
                 assert np.array_equal(run.core_local.cpu().numpy(), ref), (cfg, fl)
                 assert run.rounds == l2 and run.frontier_sizes == sizes, (cfg, fl, run.rounds, l2)
+            # sharded PeelOne, its level loop on the device (the same window, 1-word items)
+            _, km, lv, sr = oracle.peel_levels(rp_np, ci_np)
+            nz = ref[ref > 0]
+            per_level = [int((nz == k).sum()) for k in np.unique(nz)]
+            for fl in (0, pico.F_TINY_TILES, pico.F_CLAMP_CAS):
+                run = sharded.coreness_sharded_nccl(rp, ci, n, m, 0, comm, flags=fl | pico.F_LSA_EXCHANGE, algo=1)
+                torch.cuda.synchronize()
+                assert np.array_equal(run.core_local.cpu().numpy(), ref), (cfg, "peel", fl)
+                assert (run.levels, run.rounds, run.kmax) == (lv, sr, km), (cfg, fl, run.levels, run.rounds)
+                assert run.frontier_sizes == per_level
     finally:
         comm.close()
