@@ -468,6 +468,9 @@ def bench_single(args):
         res["roofline"]["traffic"] = ncu_traffic(args.config, algo, res["roofline"]["kernel"])
         res["roofline"]["l2_throughput_pct"] = ncu_slot(args.config, algo, res["roofline"]["kernel"]).get(
             "l2_throughput_pct")
+        # the binding ceiling of the dense rounds: the SM -> L2 request interface's busy share
+        res["roofline"]["l2_request_pct"] = ncu_slot(args.config, algo, res["roofline"]["kernel"]).get(
+            "l2_request_pct")
         if core_ref is None:
             core_ref = core.cpu().numpy()
         else:

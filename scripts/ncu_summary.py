@@ -28,7 +28,8 @@ SLOTS = [
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
-           "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_red.sum"]
+           "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
+           "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"gpu__time_duration.sum": {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0},
          "dram__bytes_read.sum": {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12},
          "dram__bytes_write.sum": {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}}
@@ -90,11 +91,15 @@ def main():
         if slot is None:
             continue
         a = agg.setdefault(kalgo, {}).setdefault(slot, {"dram_bytes_per_step": 0.0, "time_s": 0.0, "kernels": [],
-                                                        "l2w": 0.0})
+                                                        "l2w": 0.0, "reqw": 0.0})
         a["dram_bytes_per_step"] += vals.get("dram__bytes_read.sum", 0) + vals.get("dram__bytes_write.sum", 0)
         a["time_s"] += vals.get("gpu__time_duration.sum", 0)
         # time-weighted L2 throughput (% of peak) of the slot's kernels: the second ceiling
         a["l2w"] += vals.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", 0) * vals.get(
+            "gpu__time_duration.sum", 0)
+        # time-weighted busy share of the SM -> L2 request interface: the ceiling
+        # a dense pull round hits (profiles/r02/s3/ncu_T_pull_rounds.md)
+        a["reqw"] += vals.get("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed", 0) * vals.get(
             "gpu__time_duration.sum", 0)
         a["kernels"].append(name[:60])
     try:
@@ -106,6 +111,7 @@ def main():
         allj.setdefault(cfg, {})[kalgo] = {k: {"dram_bytes_per_step": v["dram_bytes_per_step"],
                                                "ncu_time_s": v["time_s"], "kernels": v["kernels"],
                                                "l2_throughput_pct": v["l2w"] / v["time_s"] if v["time_s"] else None,
+                                               "l2_request_pct": v["reqw"] / v["time_s"] if v["time_s"] else None,
                                                "source": rep} for k, v in slots.items()}
     with open(out, "w") as f:
         json.dump(allj, f, indent=1, sort_keys=True)
