@@ -253,6 +253,8 @@ struct Ctrl {
     alignas(128) unsigned long long q_pending;  // pushed, not fully processed
     alignas(128) unsigned long long q_snap;     // tail snapshot at the last barrier
     alignas(128) unsigned long long q_tail1;    // PeelOne: the queue's second append counter
+    alignas(128) unsigned long long nJoin;      // PeelOne rebuild: far vertices joining the near list
+    int kminJ;                                  // PeelOne rebuild: their minimum estimate
     alignas(128) unsigned long long nAlive[2];  // alive list lengths (ping-pong by level; own line: the
                                                 // scans append to these and to a queue counter at once)
     unsigned long long nFar[2];    // far list lengths (ping-pong by rebuild)

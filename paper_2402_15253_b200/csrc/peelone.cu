@@ -57,7 +57,9 @@ struct PoArgs {
     int *far1;     // holds those with estimate <= khi, far[] the others
     int khi0;      // initial window bound (INT_MAX: no far list)
     unsigned *done;  // [n/32] processed bitmap: v entered a frontier (its coreness is final)
-    long long *Q;  // run-wide queue log: (v << 32) | segment
+    long long *Q;  // run-wide queue log: (row offset << 8) | length, or (v << 32) | segment (enc_rows 0)
+    int enc_rows;  // entries hold their arc range (the drain loads no row bounds); 0 for the
+                   // end-of-level repair clamp (PICO_F_CLAMP_SUB), which needs the vertex
     unsigned long long *fsz;
     unsigned long long fsz_cap;
     unsigned long long *rtime;  // [2 fsz_cap] per scanned level: scan ns | k << 40, drain ns | sub-rounds << 40
@@ -86,8 +88,13 @@ struct PoAppend {
 // row.  Returns the number of vertices appended.
 __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v, const PoAppend ap) {
     const int lane = lane_id();
-    int ns = 0;
-    if (pred) ns = po_nseg(__ldg(a.rp + v + 1) - __ldg(a.rp + v), a.seg);
+    int ns = 0, dv = 0;
+    long long r0 = 0;
+    if (pred) {
+        r0 = __ldg(a.rp + v);
+        dv = (int)(__ldg(a.rp + v + 1) - r0);
+        ns = po_nseg(dv, a.seg);
+    }
     if (__any_sync(FULL, pred)) {
         // processed: later guards skip v.  Lanes whose vertices share a bitmap
         // word (the scan's frontier comes from id-ordered blocks) OR their bits
@@ -119,16 +126,25 @@ __device__ __forceinline__ int po_push(const PoArgs &a, bool pred, int v, const 
         }
         const int vo = __shfl_sync(FULL, v, lo);
         const int eo = __shfl_sync(FULL, excl, lo);
-        if (j < total) a.Q[base + j] = ((long long)vo << 32) | (unsigned)(j - eo);
+        if (a.enc_rows) {  // (uniform) the entry's arc range: row offset << 8 | length
+            const long long ro = __shfl_sync(FULL, r0, lo);
+            const int dvo = __shfl_sync(FULL, dv, lo);
+            const int so = (j - eo) * a.seg;
+            if (j < total) a.Q[base + j] = ((ro + so) << 8) | (long long)min(a.seg, dvo - so);
+        } else if (j < total) {
+            a.Q[base + j] = ((long long)vo << 32) | (unsigned)(j - eo);
+        }
     }
     return __popc(__ballot_sync(FULL, pred));
 }
 
 // scan of level k (parity p): alive[p] -> frontier entries in the queue, alive[p^1]
+// na_in: the near list's length when the caller knows it (the level kernel:
+// head count + rebuild joiners), else -1 (read nAlive[p])
 template <bool STATS>
 __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, long long nthreads,
-                              const PoAppend ap) {
-    const long long na = (long long)bcast_u64(&a.ctl->nAlive[p]);
+                              const PoAppend ap, long long na_in = -1) {
+    const long long na = na_in >= 0 ? na_in : (long long)bcast_u64(&a.ctl->nAlive[p]);
     const int *alive = p ? a.alive1 : a.alive0;
     int *next = p ? a.alive0 : a.alive1;
     long long iters = (na + nthreads - 1) / nthreads;
@@ -167,8 +183,13 @@ __device__ void po_scan_phase(const PoArgs &a, int k, int p, long long gthread, 
 // those that already crossed (estimate <= the old khi) are dropped.  The
 // level bound is min(near bound, far minimum).  The scanned set is exactly
 // what a full scan would find with estimate == k (nothing else changes).
-__device__ void po_rebuild_phase(const PoArgs &a, int khi_old, int khi, int fp, int p, long long gthread,
-                                 long long nthreads, bool stats) {
+// The joiners go to near[na0 + ...] through their own counter and bound
+// (nJoin, kminJ), never through nAlive[p] / kminb[p]: those are the level
+// head's inputs, and a CTA still reading the head while a faster one rebuilt
+// would otherwise see na > 0 or a lower bound, take another branch and put the
+// grid barriers out of step (a rare hang at RMAT-26 / C4).
+__device__ void po_rebuild_phase(const PoArgs &a, int khi_old, int khi, int fp, int p, long long na0,
+                                 long long gthread, long long nthreads, bool stats) {
     const long long nf = (long long)bcast_u64(&a.ctl->nFar[fp]);
     const int *far = fp ? a.far1 : a.far0;
     int *keepto = fp ? a.far0 : a.far1;
@@ -187,14 +208,14 @@ __device__ void po_rebuild_phase(const PoArgs &a, int khi_old, int khi, int fp, 
         const bool stay = valid && c > khi;
         if (join) kmin = min(kmin, c);
         if (stay) fmin = min(fmin, c);
-        warp_append(join, v, near, &a.ctl->nAlive[p]);
+        warp_append(join, v, near + na0, &a.ctl->nJoin);
         warp_append(stay, v, keepto, &a.ctl->nFar[fp ^ 1]);
     }
     fmin = warp_min(fmin);
     kmin = warp_min(kmin);
     if (lane_id() == 0) {
         if (fmin != INT_MAX) atomicMin(&a.ctl->fmin[fp ^ 1], fmin);
-        if (kmin != INT_MAX) atomicMin(&a.ctl->kminb[p], kmin);
+        if (kmin != INT_MAX) atomicMin(&a.ctl->kminJ, kmin);
         if (stats && gthread == 0) atomicAdd(&a.ctl->st_alive, (unsigned long long)nf);
     }
 }
@@ -262,11 +283,16 @@ __device__ void po_sub_phase(const PoArgs &a, int k, int p, const PoAppend ap, u
             int len = 0;
             if (i < hi) {
                 long long e = __ldcg(Qx + i);
-                int v = (int)(e >> 32);
-                int s = (int)(e & 0xffffffffll);
-                long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
-                b = r0 + (long long)s * a.seg;
-                len = (int)min((long long)a.seg, r1 - b);
+                if (a.enc_rows) {  // uniform
+                    b = e >> 8;
+                    len = (int)(e & 0xff);
+                } else {
+                    int v = (int)(e >> 32);
+                    int s = (int)(e & 0xffffffffll);
+                    long long r0 = __ldg(a.rp + v), r1 = __ldg(a.rp + v + 1);
+                    b = r0 + (long long)s * a.seg;
+                    len = (int)min((long long)a.seg, r1 - b);
+                }
             }
 #pragma unroll
             for (int j = 0; j < A; j++) u[q * A + j] = (j * 32 + lane < len) ? __ldg(a.ci + b + j * 32 + lane) : -1;
@@ -441,7 +467,7 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             // uniform: the window is exhausted (or the near list empty): rebuild
             // the far list with a doubled window
             const int khi_new = (int)max((long long)khi, min(2ll * k + 16, (long long)INT_MAX - 1));
-            po_rebuild_phase(a, khi, khi_new, fp, p, gthread, nthreads, STATS);
+            po_rebuild_phase(a, khi, khi_new, fp, p, na, gthread, nthreads, STATS);
             grid_sync(c);
             if (leader) {
                 c->nFar[fp] = 0;  // consumed; refilled at the next rebuild
@@ -449,17 +475,22 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             }
             khi = khi_new;
             fp ^= 1;
-            // the joiners lowered kminb[p]; the far minimum is the rebuilt one
+            // the joiners extend the near list and may lower its bound; the far
+            // minimum is the rebuilt one
+            na += (long long)bcast_u64(&c->nJoin);
             const long long nf2 = (long long)bcast_u64(&c->nFar[fp]);
-            k = max(k, min(bcast_i32(&c->kminb[p]), nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
+            const int kj = min(bcast_i32(&c->kminb[p]), bcast_i32(&c->kminJ));
+            k = max(k, min(kj, nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
         }
         const unsigned long long lstart = lo;
-        po_scan_phase<STATS>(a, k, p, gthread, nthreads, PoAppend{lo, y ? cb1 : cb0, y});
+        po_scan_phase<STATS>(a, k, p, gthread, nthreads, PoAppend{lo, y ? cb1 : cb0, y}, na);
         grid_sync(c);
         if (leader) ts1 = globaltimer();
         if (leader) {
             c->nAlive[p] = 0;       // alive[p] consumed; refilled at level L+1
             c->kminb[p] = INT_MAX;  // consumed at this level's head
+            c->nJoin = 0;           // read by every CTA before the scan
+            c->kminJ = INT_MAX;
         }
         for (int sub = 0;; sub++) {
             // entries appended by the previous phase through counter y: frozen,
@@ -559,6 +590,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     // the host loop keeps one alive list (no far list)
     a.khi0 = (flags & PICO_F_HOST_LOOP) ? INT_MAX : PICO_PO_KHI0;
     a.seg = po_seg(flags);
+    a.enc_rows = CLAMP_SUB ? 0 : 1;  // the repair clamp reads the vertex of every entry
     a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core;
 
     cudaError_t err;
@@ -567,6 +599,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     h.kminb[1] = INT_MAX;
     h.fmin[0] = INT_MAX;
     h.fmin[1] = INT_MAX;
+    h.kminJ = INT_MAX;
     if ((err = cudaMemcpyAsync(a.ctl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s))) return err;
     if ((err = cudaMemsetAsync(a.done, 0, sizeof(unsigned) * (size_t)((n + 31) / 32 + 1), s))) return err;
 
