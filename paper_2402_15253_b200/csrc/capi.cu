@@ -327,7 +327,9 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
                     cudaEventCreate(&r1);
                     cudaEventRecord(r0, s);
                 }
+                nvtx_push(PICO_K_OTHER);
                 e = relabel_build(rp, colidx, n, arcs, s, (char *)ws + ab, dev, (flags & PICO_F_RELABEL) != 0, &rl);
+                nvtxRangePop();
                 if (e) rc = cuda_fail(e, "relabel");
                 if (timing) cudaEventRecord(r1, s);
                 if (rl.active) {
@@ -357,7 +359,9 @@ int pico_coreness_ex(const int64_t *rowptr, const int32_t *colidx, int64_t n, in
                     cudaEventCreate(&b1);
                     cudaEventRecord(b0, s);
                 }
+                nvtx_push(PICO_K_OTHER);
                 e = relabel_back(rl, n, core_out, s, dev);
+                nvtxRangePop();
                 if (timing) cudaEventRecord(b1, s);
                 if (!e) e = cudaStreamSynchronize(s);
                 if (e) rc = cuda_fail(e, "relabel back");

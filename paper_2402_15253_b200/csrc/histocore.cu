@@ -1492,11 +1492,14 @@ size_t hc_workspace_bytes(long long n, long long arcs, uint32_t flags) {
     return hc_layout(n, arcs, flags).total;
 }
 
+// Phase slots double as NVTX ranges (always on; no-ops without a tool
+// attached): nsys / ncu --nvtx attribute every launch to its phase
 struct Timer {
     cudaStream_t s;
     bool on;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     void start(int slot) {
+        nvtx_push(slot);
         if (!on) return;
         cudaEvent_t a, b;
         cudaEventCreate(&a);
@@ -1505,6 +1508,7 @@ struct Timer {
         ev.push_back({slot, {a, b}});
     }
     void stop() {
+        nvtxRangePop();
         if (!on) return;
         cudaEventRecord(ev.back().second.second, s);
     }

@@ -8,8 +8,16 @@
 #include <vector>
 
 #include "pico.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace pico {
+
+// NVTX range of a phase slot (PICO_K_*): "pico:<slot>"
+inline void nvtx_push(int slot) {
+    static const char *names[PICO_K_COUNT] = {"pico:degree", "pico:init", "pico:rounds", "pico:sum", "pico:update",
+                                              "pico:peel", "pico:validate", "pico:relabel", "pico:edgelist"};
+    nvtxRangePushA(slot >= 0 && slot < PICO_K_COUNT ? names[slot] : "pico");
+}
 
 constexpr unsigned long long kFszCap = 1ull << 16;  // per-round sizes recorded
 

@@ -605,6 +605,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
 
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     auto tstart = [&](int slot) {
+        nvtx_push(slot);  // NVTX range of the phase (kernels.h)
         if (!(flags & PICO_F_TIMING)) return;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
@@ -613,6 +614,7 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
         ev.push_back({slot, {e0, e1}});
     };
     auto tstop = [&]() {
+        nvtxRangePop();
         if (flags & PICO_F_TIMING) cudaEventRecord(ev.back().second.second, s);
     };
 
