@@ -3,5 +3,5 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/s3x
 for r in rounds peel init edgelist; do
   timeout 300 ncu --nvtx --nvtx-include "pico:$r/" --metrics gpu__time_duration.sum --csv python scripts/one_call.py C2 > gpurun_out/s3x/nvtx_$r.csv 2>/dev/null
-  echo "$r: $(grep -o '"[a-z_:]*pico::[a-z_0-9]*' gpurun_out/s3x/nvtx_$r.csv | sort | uniq -c | tr '\n' ' ')"
+  python -c "import csv;rows=[r for r in csv.reader(open('gpurun_out/s3x/nvtx_$r.csv')) if len(r)>10 and r[0].isdigit()];print('$r',sorted(set(x[6].split('(')[0] for x in rows)))"
 done
