@@ -720,7 +720,10 @@ __global__ void __launch_bounds__(256) hc_el_count_kernel(HcArgs a, unsigned lon
 
 // warp per chunk: the scanned counts are the output offsets; 4 steps of 32
 // arcs in flight, one ballot per bucket and step
-__global__ void __launch_bounds__(256) hc_el_fill_kernel(HcArgs a, const int *src, const unsigned long long *off,
+#ifndef PICO_FILL_MINB
+#define PICO_FILL_MINB 1  // resident 256-thread CTAs per SM the fill's registers must allow (A/B)
+#endif
+__global__ void __launch_bounds__(256, PICO_FILL_MINB) hc_el_fill_kernel(HcArgs a, const int *src, const unsigned long long *off,
                                                          long long nchunk) {
     const int lane = lane_id();
     const unsigned lt = (1u << lane) - 1;
