@@ -35,7 +35,7 @@
 #include "kernels.h"
 
 #ifndef PICO_PO_KHI0
-#define PICO_PO_KHI0 32  // initial near window: vertices of degree <= 32
+#define PICO_PO_KHI0 16  // initial near window: vertices of degree <= 16 (sweep 8/16/32/64: profiles/r02/s3/po_khi0.txt)
 #endif
 #ifndef PICO_PO_THREADS
 #define PICO_PO_THREADS 512  // threads per CTA of the persistent level kernel
