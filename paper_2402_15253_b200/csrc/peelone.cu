@@ -37,6 +37,15 @@
 #ifndef PICO_PO_KHI0
 #define PICO_PO_KHI0 16  // initial near window: vertices of degree <= 16 (sweep 8/16/32/64: profiles/r02/s3/po_khi0.txt)
 #endif
+#ifndef PICO_PO_KHI_NUM  // far-list rebuild: the new window is NUM/DEN * k + ADD
+#define PICO_PO_KHI_NUM 2
+#endif
+#ifndef PICO_PO_KHI_DEN
+#define PICO_PO_KHI_DEN 1
+#endif
+#ifndef PICO_PO_KHI_ADD
+#define PICO_PO_KHI_ADD 16
+#endif
 #ifndef PICO_PO_THREADS
 #define PICO_PO_THREADS 512  // threads per CTA of the persistent level kernel
 #endif
@@ -466,7 +475,8 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
         if (nf && (k > khi || na == 0)) {
             // uniform: the window is exhausted (or the near list empty): rebuild
             // the far list with a doubled window
-            const int khi_new = (int)max((long long)khi, min(2ll * k + 16, (long long)INT_MAX - 1));
+            const int khi_new = (int)max((long long)khi, min((long long)PICO_PO_KHI_NUM * k / PICO_PO_KHI_DEN +
+                                                                 PICO_PO_KHI_ADD, (long long)INT_MAX - 1));
             po_rebuild_phase(a, khi, khi_new, fp, p, na, gthread, nthreads, STATS);
             grid_sync(c);
             if (leader) {
