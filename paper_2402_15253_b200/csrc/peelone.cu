@@ -30,6 +30,8 @@
 // clamp_dec(): atomicSub + atomicMax on overshoot (default), atomicSub + end-
 // of-level repair (PICO_F_CLAMP_SUB), CAS loop (PICO_F_CLAMP_CAS).
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -65,6 +67,7 @@ struct PoArgs {
     int *far0;     // near / far split of the alive vertices: alive[] ("near")
     int *far1;     // holds those with estimate <= khi, far[] the others
     int khi0;      // initial window bound (INT_MAX: no far list)
+    int khi_num, khi_den, khi_add;  // rebuild window num/den * k + add (PICO_PO_KHI_*; env PICO_PO_WINDOW)
     unsigned *done;  // [n/32] processed bitmap: v entered a frontier (its coreness is final)
     long long *Q;  // run-wide queue log: (row offset << 8) | length, or (v << 32) | segment (enc_rows 0)
     int enc_rows;  // entries hold their arc range (the drain loads no row bounds); 0 for the
@@ -472,12 +475,19 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
         if (na == 0 && nf == 0) break;
         k = max(k + 1, min((int)s_head[2], nf ? (int)s_head[3] : INT_MAX));
         unsigned long long ts0 = leader ? globaltimer() : 0, ts1 = 0, S0 = S;
-        if (nf && (k > khi || na == 0)) {
-            // uniform: the window is exhausted (or the near list empty): rebuild
-            // the far list with a doubled window
-            const int khi_new = (int)max((long long)khi, min((long long)PICO_PO_KHI_NUM * k / PICO_PO_KHI_DEN +
-                                                                 PICO_PO_KHI_ADD, (long long)INT_MAX - 1));
-            po_rebuild_phase(a, khi, khi_new, fp, p, na, gthread, nthreads, STATS);
+        // the window is exhausted (or the near list empty): rebuild the far
+        // list with a wider window -- repeatedly if the level's bound is still
+        // beyond the new window (every vertex of level k must be in the near
+        // list before the scan: a single rebuild whose far minimum lands above
+        // the new window left those vertices in the far list, unscanned; with
+        // a 1.5k + 16 window rule that lost 7-194 vertices per RMAT graph)
+        const long long na_head = na;
+        long long nfc = nf;
+        for (int nrb = 0; nfc && (k > khi || na == 0); nrb++) {  // uniform
+            if (nrb) grid_sync(c);  // the leader's resets of the previous pass first
+            const int khi_new = (int)max((long long)khi, min((long long)a.khi_num * k / a.khi_den + a.khi_add,
+                                                             (long long)INT_MAX - 1));
+            po_rebuild_phase(a, khi, khi_new, fp, p, na_head, gthread, nthreads, STATS);
             grid_sync(c);
             if (leader) {
                 c->nFar[fp] = 0;  // consumed; refilled at the next rebuild
@@ -487,10 +497,10 @@ __global__ void __launch_bounds__(PICO_PO_THREADS, PICO_PO_PER) po_levels_kernel
             fp ^= 1;
             // the joiners extend the near list and may lower its bound; the far
             // minimum is the rebuilt one
-            na += (long long)bcast_u64(&c->nJoin);
-            const long long nf2 = (long long)bcast_u64(&c->nFar[fp]);
+            na = na_head + (long long)bcast_u64(&c->nJoin);
+            nfc = (long long)bcast_u64(&c->nFar[fp]);
             const int kj = min(bcast_i32(&c->kminb[p]), bcast_i32(&c->kminJ));
-            k = max(k, min(kj, nf2 ? bcast_i32(&c->fmin[fp]) : INT_MAX));
+            k = max(k, min(kj, nfc ? bcast_i32(&c->fmin[fp]) : INT_MAX));
         }
         const unsigned long long lstart = lo;
         po_scan_phase<STATS>(a, k, p, gthread, nthreads, PoAppend{lo, y ? cb1 : cb0, y}, na);
@@ -599,6 +609,17 @@ static cudaError_t po_run_t(const long long *rp, const int *ci, long long n, lon
     a.Q = (long long *)p;
     // the host loop keeps one alive list (no far list)
     a.khi0 = (flags & PICO_F_HOST_LOOP) ? INT_MAX : PICO_PO_KHI0;
+    a.khi_num = PICO_PO_KHI_NUM;
+    a.khi_den = PICO_PO_KHI_DEN;
+    a.khi_add = PICO_PO_KHI_ADD;
+    if (const char *w = getenv("PICO_PO_WINDOW")) {  // "num/den+add": tests and A/B runs
+        int nu = 0, de = 0, ad = 0;
+        if (sscanf(w, "%d/%d+%d", &nu, &de, &ad) == 3 && nu >= de && de > 0 && ad > 0) {
+            a.khi_num = nu;
+            a.khi_den = de;
+            a.khi_add = ad;
+        }
+    }
     a.seg = po_seg(flags);
     a.enc_rows = CLAMP_SUB ? 0 : 1;  // the repair clamp reads the vertex of every entry
     a.rp = rp; a.ci = ci; a.n = (int)n; a.core = core;
