@@ -37,7 +37,7 @@
 #include "kernels.h"
 
 #ifndef PICO_PO_KHI0
-#define PICO_PO_KHI0 16  // initial near window: vertices of degree <= 16 (sweep 8/16/32/64: profiles/r02/s3/po_khi0.txt)
+#define PICO_PO_KHI0 32  // initial near window: vertices of degree <= 32 (16 was 2-4 % faster in a sweep, profiles/r02/s3/po_khi0.txt, but its first bench run hit a fault not reproduced since: kept at the long-validated 32)
 #endif
 #ifndef PICO_PO_KHI_NUM  // far-list rebuild: the new window is NUM/DEN * k + ADD
 #define PICO_PO_KHI_NUM 2
